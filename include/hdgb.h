@@ -1,0 +1,136 @@
+/*
+ * hdgb.h — C ABI of the B200-native LDG-H trace-operator hot path
+ * (arXiv 2007.11891, Alg. 2/3 operator, Alg. 4 face-wise preconditioner, PCG).
+ *
+ * Plain C types only: device pointers are `double*` into one contiguous
+ * "all-face" vector in the reference `pack_all` order (hdgbox/mesh.py:324-326):
+ * direction blocks d = 0,1,2 of shape (n_faces[d], n, n), C order, tangential
+ * axes in increasing coordinate order (mesh.py:215-221).  Streams are
+ * `cudaStream_t` passed as `void*` (NULL = legacy default stream).
+ *
+ * The reference package (`hdgbox`, pure Python/numpy) has no native FFI of
+ * its own; each entry point below replaces the Python function cited next to
+ * it, and the Python shims in paper_2007_11891_b200/ bind them via ctypes
+ * (see INTEGRATION.md).  No exceptions cross the ABI: every call returns an
+ * hdgb_status; hdgb_last_error() gives the message of the last failure on the
+ * calling thread.
+ */
+#ifndef HDGB_H
+#define HDGB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HDGB_OK = 0,
+  HDGB_EINVAL = 1,      /* -> ValueError (shapes, arguments, config)                   */
+  HDGB_EBREAKDOWN = 2,  /* -> FloatingPointError (CG curvature <= 0 / non-finite)     */
+  HDGB_ECUDA = 3,       /* -> RuntimeError (CUDA runtime failure)                      */
+  HDGB_ENCCL = 4,       /* -> RuntimeError (collective failure; reserved)              */
+  HDGB_ENONFINITE = 5   /* -> FloatingPointError (non-finite residual)                 */
+} hdgb_status;
+
+/* face / box-side kinds (mesh.py:31-33 plus slab-interface kinds for multi-GPU) */
+enum {
+  HDGB_INTERIOR = 0,
+  HDGB_DIRICHLET = 1,
+  HDGB_NEUMANN = 2,
+  HDGB_HALO_OWNED = 3,  /* slab interface plane whose unknowns this rank owns in dots  */
+  HDGB_HALO_PEER = 4    /* slab interface plane owned by the neighbouring rank         */
+};
+
+enum { HDGB_PLAIN = 0, HDGB_TRANSFORMED = 1 };                  /* Alg. 2 / Alg. 3   */
+enum { HDGB_PREC_NONE = 0, HDGB_PREC_BLOCK = 1,                 /* Alg. 4            */
+       HDGB_PREC_DIAG_NODAL = 2, HDGB_PREC_DIAG_EIGEN = 3 };
+
+typedef struct hdgb_ctx hdgb_ctx;
+
+/* Mesh + basis description.  All pointers are HOST pointers, copied at create. */
+typedef struct {
+  int32_t n_el[3];          /* local element counts n1, n2, n3                         */
+  int32_t p;                /* polynomial degree, 1..16                                 */
+  double lam;               /* Helmholtz lambda >= 0                                    */
+  const double* widths[3];  /* per-axis element widths, length n_el[d]                  */
+  int32_t side_kind[6];     /* x1lo, x1hi, x2lo, x2hi, x3lo, x3hi: HDGB_* kinds         */
+  const double* S;          /* n*n, S[i*n+a]   (basis.py: generalized eigenvectors)     */
+  const double* B_S;        /* n*2, B_S[a*2+l] (basis.py: fused face->eigen map)        */
+  const double* Lambda;     /* n                                                        */
+  const double* weights;    /* n   GLL weights (lumped mass diagonal)                   */
+  const double* GCC_diag;   /* 2   diag(G + C^T M^-1 C)                                 */
+  const double* dz_inv;     /* n^3 shared inverse eigenvalue scale, uniform grids only;
+                               NULL = computed on the device per element                */
+  int32_t device;           /* CUDA device ordinal                                      */
+} hdgb_desc;
+
+const char* hdgb_last_error(void);
+const char* hdgb_version(void);
+
+/* OperatorContext (operator.py:129-192) + preconditioner builds (preconditioner.py:79-94,
+ * 139-151, 178-204): uploads tables, allocates scratch. */
+int hdgb_ctx_create(const hdgb_desc* desc, hdgb_ctx** out);
+int hdgb_ctx_destroy(hdgb_ctx* ctx);
+int64_t hdgb_ctx_n_all(const hdgb_ctx* ctx);      /* all-face doubles (pack_all length)   */
+int64_t hdgb_ctx_n_unknown(const hdgb_ctx* ctx);  /* mesh.n_trace_unknowns(p)             */
+int64_t hdgb_ctx_n_faces(const hdgb_ctx* ctx, int d);
+
+/* r = K u on all faces (hdg_op_3d, operator.py:261-267 / hdg_op_3d_transformed 270-276).
+ * u and r must not alias.  Dirichlet rows are evaluated like the reference. */
+int hdgb_op_apply(hdgb_ctx* ctx, int variant, const double* u, double* r, void* stream);
+
+/* Same with HOST buffers (pinned for full PCIe speed): copies in, applies, copies out,
+ * synchronizes.  The e2e path of bench.py. */
+int hdgb_op_apply_host(hdgb_ctx* ctx, int variant, const double* u_host, double* r_host, void* stream);
+
+/* out = (A (x) A) in on every face block (transform_faces, operator.py:279-285).
+ * A_host: n*n host matrix, row-major A[i*n+j]. */
+int hdgb_face_transform(hdgb_ctx* ctx, const double* A_host, const double* in, double* out, void* stream);
+
+/* z = P r on all faces, Dirichlet faces zero (BlockPreconditioner.apply preconditioner.py:96-108,
+ * DiagonalPreconditioner.apply 153-160, transformed_preconditioner 195-204). */
+int hdgb_prec_apply(hdgb_ctx* ctx, int kind, const double* r, double* z, void* stream);
+
+/* z = r / diag_all entrywise with a caller-supplied all-face diagonal, Dirichlet faces zero
+ * (DiagonalPreconditioner built from arbitrary face diagonals, preconditioner.py:139-165). */
+int hdgb_diag_apply(hdgb_ctx* ctx, const double* diag_all, const double* r, double* z, void* stream);
+
+/* Expand the preconditioner table of `kind` to an all-face vector: BLOCK -> y^-1 (Dirichlet
+ * faces 1.0, preconditioner.py:91-93), DIAG_NODAL / DIAG_EIGEN -> the diagonal (Dirichlet 1.0). */
+int hdgb_prec_table(hdgb_ctx* ctx, int kind, double* out_all, void* stream);
+
+/* pack_unknowns / unpack_unknowns (mesh.py:318-321, 341-351) */
+int hdgb_pack(hdgb_ctx* ctx, const double* all, double* packed, void* stream);
+int hdgb_unpack(hdgb_ctx* ctx, const double* packed, double* all, void* stream);
+/* zero the Dirichlet face blocks in place (FluxField.zero_dirichlet, mesh.py:242-246) */
+int hdgb_zero_dirichlet(hdgb_ctx* ctx, double* all, void* stream);
+
+/* Fused device PCG (solver.py:282-321) on the all-face layout, Dirichlet slots held at 0.
+ * F: all-face RHS (Dirichlet slots ignored); x: all-face initial guess in, solution out.
+ * Results are written to the host ints/doubles after a stream sync.  Returns
+ * HDGB_EBREAKDOWN / HDGB_ENONFINITE where the reference raises FloatingPointError. */
+int hdgb_pcg(hdgb_ctx* ctx, int variant, int prec, const double* F, double* x, double rtol, double atol,
+             int32_t max_iters, int32_t* iters, double* relres, int32_t* converged, void* stream);
+
+/* Generic FP64 vector kernels for pcg() with arbitrary callables (solver.py:282-321). */
+int64_t hdgb_dot_scratch_doubles(void);
+/* *result_dev = sum_i x_i y_i (deterministic fixed-order reduction). */
+int hdgb_vec_dot(const double* x, const double* y, int64_t n, double* scratch_dev, double* result_dev,
+                 void* stream);
+/* out = a*x + b*y (out may alias x or y). */
+int hdgb_vec_axpby(int64_t n, double a, const double* x, double b, const double* y, double* out, void* stream);
+
+/* Slab halo support (multi-GPU): pack the local x-face plane `plane`
+ * (0 or n1) of an all-face vector into a contiguous n2*n3*n*n buffer, and add such a
+ * buffer back into the plane. */
+int hdgb_halo_pack(hdgb_ctx* ctx, const double* all, int plane, double* buf, void* stream);
+int hdgb_halo_add(hdgb_ctx* ctx, double* all, int plane, const double* buf, void* stream);
+
+/* Number of kernels launched by this ctx so far (evidence counter for bench.py). */
+int64_t hdgb_ctx_launches(const hdgb_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HDGB_H */

@@ -1,0 +1,476 @@
+// C ABI (include/hdgb.h): context lifetime, entry points, and the fused PCG driver.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hdgb_internal.cuh"
+
+namespace hdgb {
+cudaError_t launch_cg_init(hdgb_ctx* c, int kind, cudaStream_t s);
+cudaError_t launch_reduce_pw(hdgb_ctx* c, cudaStream_t s);
+cudaError_t launch_p_update(hdgb_ctx* c, cudaStream_t s, cudaGraphConditionalHandle loop, int has_loop);
+cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* scratch, double* result, cudaStream_t s);
+cudaError_t launch_axpby(int64_t n, double a, const double* x, double b, const double* y, double* out, cudaStream_t s);
+cudaError_t launch_pack(hdgb_ctx* c, int mode, const double* in, double* out, cudaStream_t s);
+cudaError_t launch_halo(hdgb_ctx* c, int mode, int plane, double* all, double* buf, cudaStream_t s);
+cudaError_t launch_diag_user(hdgb_ctx* c, const double* diag, const double* in, double* out, cudaStream_t s);
+cudaError_t launch_expand_table(hdgb_ctx* c, int kind, double* out, cudaStream_t s);
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  return HDGB_ECUDA;
+}
+static int einval(const std::string& m) {
+  g_err = m;
+  return HDGB_EINVAL;
+}
+enum { V_X = 0, V_R = 1, V_Z = 2, V_P = 3, V_W = 4, V_F = 5 };
+}  // namespace hdgb
+
+using namespace hdgb;
+
+extern "C" {
+
+const char* hdgb_last_error(void) { return g_err.c_str(); }
+const char* hdgb_version(void) { return "hdgb 0.1 (sm_100a)"; }
+
+int64_t hdgb_ctx_n_all(const hdgb_ctx* c) { return c ? c->n_all : -1; }
+int64_t hdgb_ctx_n_unknown(const hdgb_ctx* c) { return c ? c->n_unknown : -1; }
+int64_t hdgb_ctx_n_faces(const hdgb_ctx* c, int d) { return (c && d >= 0 && d < 3) ? c->g.nf[d] : -1; }
+int64_t hdgb_ctx_launches(const hdgb_ctx* c) { return c ? c->launches : -1; }
+int64_t hdgb_dot_scratch_doubles(void) { return 2 * HDGB_RED_BLOCKS + 8; }
+
+static void free_ctx(hdgb_ctx* c) {
+  if (!c) return;
+  for (auto& row : c->graph)
+    for (auto& gx : row)
+      if (gx) cudaGraphExecDestroy(gx);
+  double* bufs[] = {c->d_tab, c->d_dz, c->d_widths, c->d_yinv_cls, c->d_y_cls, c->d_dn_cls, c->d_yinv_full,
+                    c->d_y_full, c->d_dn_full, c->d_xbuf, c->d_facedot, c->d_part, c->d_A, c->d_vec, c->d_io};
+  for (double* b : bufs)
+    if (b) cudaFree(b);
+  if (c->d_tickets) cudaFree(c->d_tickets);
+  if (c->d_st) cudaFree(c->d_st);
+  if (c->h_st) cudaFreeHost(c->h_st);
+  if (c->ev_in) cudaEventDestroy(c->ev_in);
+  if (c->ev_out) cudaEventDestroy(c->ev_out);
+  if (c->s) cudaStreamDestroy(c->s);
+  delete c;
+}
+
+int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
+  if (!d || !out) return einval("null argument");
+  *out = nullptr;
+  if (d->p < 1 || d->p > HDGB_MAX_N - 1) return einval("polynomial degree must lie in 1..16");
+  for (int q = 0; q < 3; ++q)
+    if (d->n_el[q] < 1) return einval("need three element counts, each >= 1");
+  if (!(d->lam >= 0.0)) return einval("the Helmholtz parameter must be non-negative");
+  if (!d->S || !d->B_S || !d->Lambda || !d->weights || !d->GCC_diag) return einval("basis tables missing");
+  for (int q = 0; q < 3; ++q)
+    if (!d->widths[q]) return einval("element widths missing");
+  for (int q = 0; q < 6; ++q)
+    if (d->side_kind[q] < HDGB_DIRICHLET || d->side_kind[q] > HDGB_HALO_PEER)
+      return einval("side kinds must be dirichlet/neumann/halo");
+
+  hdgb_ctx* c = new hdgb_ctx();
+  c->dev = d->device;
+  if (cudaSetDevice(c->dev) != cudaSuccess) {
+    delete c;
+    return einval("invalid CUDA device");
+  }
+  const int N = d->p + 1, N2 = N * N;
+  c->N = N;
+  c->p = d->p;
+  c->lam = d->lam;
+  Geo& g = c->g;
+  g.n1 = d->n_el[0];
+  g.n2 = d->n_el[1];
+  g.n3 = d->n_el[2];
+  g.ne = (int64_t)g.n1 * g.n2 * g.n3;
+  g.nf[0] = (int64_t)(g.n1 + 1) * g.n2 * g.n3;
+  g.nf[1] = (int64_t)g.n1 * (g.n2 + 1) * g.n3;
+  g.nf[2] = (int64_t)g.n1 * g.n2 * (g.n3 + 1);
+  g.foff[0] = 0;
+  g.foff[1] = g.nf[0];
+  g.foff[2] = g.nf[0] + g.nf[1];
+  for (int q = 0; q < 6; ++q) g.kind[q] = d->side_kind[q];
+  c->nfaces = g.nf[0] + g.nf[1] + g.nf[2];
+  c->n_all = c->nfaces * N2;
+  int64_t unk = 0;
+  for (int q = 0; q < 3; ++q) {
+    int nd = q == 0 ? g.n1 : (q == 1 ? g.n2 : g.n3);
+    int64_t planes = nd + 1 - (g.kind[2 * q] == HDGB_DIRICHLET) - (g.kind[2 * q + 1] == HDGB_DIRICHLET);
+    unk += g.nf[q] / (nd + 1) * planes;
+  }
+  c->n_unknown = unk * N2;
+
+  // widths + metric terms (mesh.py:46-56)
+  std::vector<double> wid;
+  bool uniform = true;
+  for (int q = 0; q < 3; ++q) {
+    int nd = q == 0 ? g.n1 : (q == 1 ? g.n2 : g.n3);
+    for (int i = 0; i < nd; ++i) {
+      double h = d->widths[q][i];
+      if (!(h > 0.0)) {
+        delete c;
+        return einval("element widths must be positive");
+      }
+      wid.push_back(h);
+      if (h != d->widths[q][0]) uniform = false;
+    }
+  }
+  c->uniform = uniform && d->dz_inv != nullptr;
+  {
+    double h1 = d->widths[0][0], h2 = d->widths[1][0], h3 = d->widths[2][0];
+    double a0 = h1 * h2 * h3 / 8.0, t1 = 2.0 / h1, t2 = 2.0 / h2, t3 = 2.0 / h3;
+    c->al_u[0] = a0;
+    c->al_u[1] = a0 * (t1 * t1);
+    c->al_u[2] = a0 * (t2 * t2);
+    c->al_u[3] = a0 * (t3 * t3);
+  }
+  // GCC must be diagonal was checked by the host (operator.py:154-156); tables:
+  TabOff to;
+  to.set(N);
+  std::vector<double> tab(to.total, 0.0);
+  for (int a = 0; a < N; ++a) {
+    tab[to.BS + 2 * a] = d->B_S[2 * a];
+    tab[to.BS + 2 * a + 1] = d->B_S[2 * a + 1];
+    tab[to.w + a] = d->weights[a];
+    tab[to.Lam + a] = d->Lambda[a];
+    for (int i = 0; i < N; ++i) {
+      double s = d->S[i * N + a];
+      tab[to.T + a * N + i] = s * d->weights[i];   // T = S^T M   (operator.py:150)
+      tab[to.MS + i * N + a] = d->weights[i] * s;  // MS = M S    (operator.py:151)
+      tab[to.S + i * N + a] = s;
+      tab[to.St + a * N + i] = s;
+    }
+  }
+  tab[to.gcc] = d->GCC_diag[0];
+  tab[to.gcc + 1] = d->GCC_diag[1];
+
+  int rc = HDGB_OK;
+#define CK(call)                          \
+  do {                                    \
+    cudaError_t _e = (call);              \
+    if (_e != cudaSuccess) {              \
+      rc = cuda_fail(_e, #call);          \
+      free_ctx(c);                        \
+      return rc;                          \
+    }                                     \
+  } while (0)
+  CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
+  CK(cudaMalloc(&c->d_tab, sizeof(double) * to.total));
+  CK(cudaMemcpy(c->d_tab, tab.data(), sizeof(double) * to.total, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&c->d_widths, sizeof(double) * wid.size()));
+  CK(cudaMemcpy(c->d_widths, wid.data(), sizeof(double) * wid.size(), cudaMemcpyHostToDevice));
+  if (c->uniform) {
+    CK(cudaMalloc(&c->d_dz, sizeof(double) * N2 * N));
+    CK(cudaMemcpy(c->d_dz, d->dz_inv, sizeof(double) * N2 * N, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&c->d_y_cls, sizeof(double) * 9 * N2));
+    CK(cudaMalloc(&c->d_yinv_cls, sizeof(double) * 9 * N2));
+    CK(cudaMalloc(&c->d_dn_cls, sizeof(double) * 9 * N2));
+  } else {
+    CK(cudaMalloc(&c->d_y_full, sizeof(double) * c->n_all));
+    CK(cudaMalloc(&c->d_yinv_full, sizeof(double) * c->n_all));
+    CK(cudaMalloc(&c->d_dn_full, sizeof(double) * c->n_all));
+  }
+  // scratch for the two-party face assembly: xbuf face stride padded to 128 B
+  c->xstride = ((int64_t)N2 + 15) / 16 * 16;
+  CK(cudaMalloc(&c->d_xbuf, sizeof(double) * c->xstride * c->nfaces));
+  CK(cudaMalloc(&c->d_tickets, sizeof(uint32_t) * c->nfaces));
+  CK(cudaMemset(c->d_tickets, 0, sizeof(uint32_t) * c->nfaces));
+  CK(cudaMalloc(&c->d_facedot, sizeof(double) * c->nfaces));
+  CK(cudaMalloc(&c->d_part, sizeof(double) * 4 * HDGB_RED_BLOCKS + 64));
+  CK(cudaMalloc(&c->d_A, sizeof(double) * N2));
+  CK(cudaMalloc(&c->d_st, sizeof(CGState)));
+  CK(cudaMemset(c->d_st, 0, sizeof(CGState)));
+  CK(cudaMallocHost(&c->h_st, sizeof(CGState)));
+  memset(c->h_st, 0, sizeof(CGState));
+  CK(launch_build_tables(c, c->s));
+  CK(cudaStreamSynchronize(c->s));
+  // validate the preconditioner diagonals on unknown faces (preconditioner.py:89-90, 146-147)
+  if (c->uniform) {
+    std::vector<double> y(9 * N2), dn(9 * N2);
+    CK(cudaMemcpy(y.data(), c->d_y_cls, sizeof(double) * 9 * N2, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(dn.data(), c->d_dn_cls, sizeof(double) * 9 * N2, cudaMemcpyDeviceToHost));
+    for (int q = 0; q < 3; ++q)
+      for (int cls = 0; cls < 3; ++cls) {
+        int nd = q == 0 ? g.n1 : (q == 1 ? g.n2 : g.n3);
+        bool used;
+        if (cls == 0) used = nd > 1 || g.kind[2 * q] >= HDGB_HALO_OWNED || g.kind[2 * q + 1] >= HDGB_HALO_OWNED;
+        else used = g.kind[2 * q + cls - 1] == HDGB_NEUMANN;
+        if (!used) continue;
+        for (int t = 0; t < N2; ++t)
+          if (!(y[(q * 3 + cls) * N2 + t] > 0.0) || !(dn[(q * 3 + cls) * N2 + t] > 0.0)) {
+            free_ctx(c);
+            return einval("non-positive face block entry; invalid tau_hat/lambda combination");
+          }
+      }
+  } else {
+    std::vector<double> y(c->n_all);
+    CK(cudaMemcpy(y.data(), c->d_y_full, sizeof(double) * c->n_all, cudaMemcpyDeviceToHost));
+    for (int64_t fid = 0; fid < c->nfaces; ++fid) {
+      int q = fid >= g.foff[2] ? 2 : (fid >= g.foff[1] ? 1 : 0);
+      int plane, t1, t2;
+      face_coords(g, q, fid - g.foff[q], plane, t1, t2);
+      if (face_kind(g, q, plane) == HDGB_DIRICHLET) continue;
+      for (int t = 0; t < N2; ++t)
+        if (!(y[fid * N2 + t] > 0.0)) {
+          free_ctx(c);
+          return einval("non-positive face block entry; invalid tau_hat/lambda combination");
+        }
+    }
+  }
+#undef CK
+  *out = c;
+  return HDGB_OK;
+}
+
+int hdgb_ctx_destroy(hdgb_ctx* c) {
+  if (!c) return einval("null context");
+  cudaSetDevice(c->dev);
+  cudaStreamSynchronize(c->s);
+  free_ctx(c);
+  return HDGB_OK;
+}
+
+int hdgb_op_apply(hdgb_ctx* c, int variant, const double* u, double* r, void* stream) {
+  if (!c || !u || !r) return einval("null argument");
+  if (variant != HDGB_PLAIN && variant != HDGB_TRANSFORMED) return einval("unknown operator variant");
+  if (u == r) return einval("input and output must not alias");
+  HDGB_CUDA(launch_op(c, variant, MODE_APPLY, u, r, (cudaStream_t)stream));
+  return HDGB_OK;
+}
+
+int hdgb_op_apply_host(hdgb_ctx* c, int variant, const double* u_host, double* r_host, void* stream) {
+  if (!c || !u_host || !r_host) return einval("null argument");
+  if (variant != HDGB_PLAIN && variant != HDGB_TRANSFORMED) return einval("unknown operator variant");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!c->d_io) HDGB_CUDA(cudaMalloc(&c->d_io, sizeof(double) * 2 * c->n_all));
+  const size_t bytes = sizeof(double) * c->n_all;
+  HDGB_CUDA(cudaMemcpyAsync(c->d_io, u_host, bytes, cudaMemcpyHostToDevice, s));
+  HDGB_CUDA(launch_op(c, variant, MODE_APPLY, c->d_io, c->d_io + c->n_all, s));
+  HDGB_CUDA(cudaMemcpyAsync(r_host, c->d_io + c->n_all, bytes, cudaMemcpyDeviceToHost, s));
+  HDGB_CUDA(cudaStreamSynchronize(s));
+  return HDGB_OK;
+}
+
+int hdgb_face_transform(hdgb_ctx* c, const double* A_host, const double* in, double* out, void* stream) {
+  if (!c || !A_host || !in || !out) return einval("null argument");
+  if (in == out) return einval("input and output must not alias");
+  cudaStream_t s = (cudaStream_t)stream;
+  // stage A through the ctx (pageable copy is synchronous w.r.t. the host)
+  HDGB_CUDA(cudaMemcpyAsync(c->d_A, A_host, sizeof(double) * c->N * c->N, cudaMemcpyHostToDevice, s));
+  HDGB_CUDA(launch_face_transform(c, c->d_A, in, out, s));
+  return HDGB_OK;
+}
+
+int hdgb_prec_apply(hdgb_ctx* c, int kind, const double* r, double* z, void* stream) {
+  if (!c || !r || !z) return einval("null argument");
+  if (kind < HDGB_PREC_NONE || kind > HDGB_PREC_DIAG_EIGEN) return einval("unknown preconditioner kind");
+  HDGB_CUDA(launch_prec(c, kind, r, z, (cudaStream_t)stream));
+  return HDGB_OK;
+}
+
+// debug hook (not part of the public header): CG-mode operator + per-face dots
+int hdgb_debug_op_cg(hdgb_ctx* c, int variant, const double* u, double* r, double* facedot_out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  HDGB_CUDA(cudaMemsetAsync(c->d_st, 0, sizeof(CGState), s));
+  HDGB_CUDA(launch_op(c, variant, MODE_CG, u, r, s));
+  HDGB_CUDA(cudaMemcpyAsync(facedot_out, c->d_facedot, sizeof(double) * c->nfaces, cudaMemcpyDeviceToDevice, s));
+  return HDGB_OK;
+}
+
+int hdgb_diag_apply(hdgb_ctx* c, const double* diag_all, const double* r, double* z, void* stream) {
+  if (!c || !diag_all || !r || !z) return einval("null argument");
+  HDGB_CUDA(launch_diag_user(c, diag_all, r, z, (cudaStream_t)stream));
+  return HDGB_OK;
+}
+
+int hdgb_prec_table(hdgb_ctx* c, int kind, double* out_all, void* stream) {
+  if (!c || !out_all) return einval("null argument");
+  if (kind != HDGB_PREC_BLOCK && kind != HDGB_PREC_DIAG_NODAL && kind != HDGB_PREC_DIAG_EIGEN)
+    return einval("preconditioner kind has no table");
+  HDGB_CUDA(launch_expand_table(c, kind, out_all, (cudaStream_t)stream));
+  return HDGB_OK;
+}
+
+int hdgb_pack(hdgb_ctx* c, const double* all, double* packed, void* stream) {
+  if (!c || !all || !packed) return einval("null argument");
+  HDGB_CUDA(launch_pack(c, 0, all, packed, (cudaStream_t)stream));
+  return HDGB_OK;
+}
+int hdgb_unpack(hdgb_ctx* c, const double* packed, double* all, void* stream) {
+  if (!c || !all || !packed) return einval("null argument");
+  HDGB_CUDA(launch_pack(c, 1, packed, all, (cudaStream_t)stream));
+  return HDGB_OK;
+}
+int hdgb_zero_dirichlet(hdgb_ctx* c, double* all, void* stream) {
+  if (!c || !all) return einval("null argument");
+  HDGB_CUDA(launch_pack(c, 2, all, all, (cudaStream_t)stream));
+  return HDGB_OK;
+}
+
+int hdgb_halo_pack(hdgb_ctx* c, const double* all, int plane, double* buf, void* stream) {
+  if (!c || !all || !buf || (plane != 0 && plane != c->g.n1)) return einval("bad halo arguments");
+  HDGB_CUDA(launch_halo(c, 0, plane, const_cast<double*>(all), buf, (cudaStream_t)stream));
+  return HDGB_OK;
+}
+int hdgb_halo_add(hdgb_ctx* c, double* all, int plane, const double* buf, void* stream) {
+  if (!c || !all || !buf || (plane != 0 && plane != c->g.n1)) return einval("bad halo arguments");
+  HDGB_CUDA(launch_halo(c, 1, plane, all, const_cast<double*>(buf), (cudaStream_t)stream));
+  return HDGB_OK;
+}
+
+int hdgb_vec_dot(const double* x, const double* y, int64_t n, double* scratch, double* result, void* stream) {
+  if (!x || !y || !scratch || !result || n < 0) return einval("bad dot arguments");
+  if (n == 0) {
+    HDGB_CUDA(cudaMemsetAsync(result, 0, sizeof(double), (cudaStream_t)stream));
+    return HDGB_OK;
+  }
+  HDGB_CUDA(launch_dot(x, y, n, scratch, result, (cudaStream_t)stream));
+  return HDGB_OK;
+}
+
+int hdgb_vec_axpby(int64_t n, double a, const double* x, double b, const double* y, double* out, void* stream) {
+  if (!x || !y || !out || n < 0) return einval("bad axpby arguments");
+  if (n == 0) return HDGB_OK;
+  HDGB_CUDA(launch_axpby(n, a, x, b, y, out, (cudaStream_t)stream));
+  return HDGB_OK;
+}
+
+// One PCG iteration's kernels (solver.py:303-320) on ctx->s.
+static cudaError_t enqueue_iteration(hdgb_ctx* c, int variant, int prec, cudaGraphConditionalHandle h, int has_loop) {
+  double* v = c->d_vec;
+  const int64_t n = c->n_all;
+  cudaError_t e;
+  if ((e = launch_op(c, variant, MODE_CG, v + V_P * n, v + V_W * n, c->s)) != cudaSuccess) return e;  // w = K p, <p,w>
+  if ((e = launch_reduce_pw(c, c->s)) != cudaSuccess) return e;                                      // alpha
+  if ((e = launch_cg_update(c, prec, c->s)) != cudaSuccess) return e;  // x,r update; z = P r; ||r||, <r,z>
+  return launch_p_update(c, c->s, h, has_loop);                        // p = z + beta p; loop control
+}
+
+// Build (once per variant/prec) a graph whose conditional WHILE node runs PCG iterations
+// until the device state says done: no host round trip per iteration.
+static int build_graph(hdgb_ctx* c, int variant, int prec) {
+  cudaGraph_t graph;
+  HDGB_CUDA(cudaGraphCreate(&graph, 0));
+  cudaGraphConditionalHandle h;
+  cudaError_t e = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    return cuda_fail(e, "cudaGraphConditionalHandleCreate");
+  }
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  e = cudaGraphAddNode(&node, graph, nullptr, 0, &cp);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    return cuda_fail(e, "cudaGraphAddNode(conditional)");
+  }
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  e = cudaStreamBeginCaptureToGraph(c->s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    return cuda_fail(e, "cudaStreamBeginCaptureToGraph");
+  }
+  cudaError_t ke = enqueue_iteration(c, variant, prec, h, 1);
+  cudaGraph_t captured;
+  e = cudaStreamEndCapture(c->s, &captured);
+  if (ke != cudaSuccess || e != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    return cuda_fail(ke != cudaSuccess ? ke : e, "PCG iteration capture");
+  }
+  cudaGraphExec_t exec;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+  c->graph[variant][prec] = exec;
+  return HDGB_OK;
+}
+
+int hdgb_pcg(hdgb_ctx* c, int variant, int prec, const double* F, double* x, double rtol, double atol,
+             int32_t max_iters, int32_t* iters, double* relres, int32_t* converged, void* stream) {
+  if (!c || !F || !x || !iters || !relres || !converged) return einval("null argument");
+  if (variant != HDGB_PLAIN && variant != HDGB_TRANSFORMED) return einval("unknown operator variant");
+  if (prec < HDGB_PREC_NONE || prec > HDGB_PREC_DIAG_EIGEN) return einval("unknown preconditioner kind");
+  if (max_iters < 1) return einval("max_iters must be at least 1");
+  cudaStream_t us = (cudaStream_t)stream;
+  const int64_t n = c->n_all;
+  const size_t bytes = sizeof(double) * n;
+  if (!c->d_vec) HDGB_CUDA(cudaMalloc(&c->d_vec, 6 * bytes));
+  double* v = c->d_vec;
+  // order after the caller's stream
+  HDGB_CUDA(cudaEventRecord(c->ev_in, us));
+  HDGB_CUDA(cudaStreamWaitEvent(c->s, c->ev_in, 0));
+  HDGB_CUDA(cudaMemcpyAsync(v + V_F * n, F, bytes, cudaMemcpyDeviceToDevice, c->s));
+  HDGB_CUDA(cudaMemcpyAsync(v + V_X * n, x, bytes, cudaMemcpyDeviceToDevice, c->s));
+  HDGB_CUDA(launch_pack(c, 2, v + V_X * n, v + V_X * n, c->s));  // unknowns only (unpack_unknowns)
+  CGState* h = c->h_st;
+  memset(h, 0, sizeof(CGState));
+  h->rtol = rtol;
+  h->atol = atol;
+  h->max_iters = max_iters;
+  HDGB_CUDA(cudaMemcpyAsync(c->d_st, h, sizeof(CGState), cudaMemcpyHostToDevice, c->s));
+  // r = F - K x0; z = P r; p = z; norm0, rho (solver.py:290-302)
+  HDGB_CUDA(launch_op(c, variant, MODE_APPLY, v + V_X * n, v + V_W * n, c->s));
+  HDGB_CUDA(launch_cg_init(c, prec, c->s));
+  HDGB_CUDA(cudaMemcpyAsync(h, c->d_st, sizeof(CGState), cudaMemcpyDeviceToHost, c->s));
+  HDGB_CUDA(cudaStreamSynchronize(c->s));
+  if (h->status == HDGB_ENONFINITE) return (set_error("non-finite initial residual"), HDGB_ENONFINITE);
+  if (!h->done) {
+    const char* mode = getenv("HDGB_PCG_LOOP");
+    bool use_graph = !(mode && strcmp(mode, "host") == 0);
+    if (use_graph) {
+      if (!c->graph[variant][prec]) {
+        int rc = build_graph(c, variant, prec);
+        if (rc != HDGB_OK) return rc;
+      }
+      HDGB_CUDA(cudaGraphLaunch(c->graph[variant][prec], c->s));
+      c->launches += 4;  // per iteration (counted again below)
+    } else {
+      // host-driven loop (debug): one iteration per round trip
+      for (int it = 0; it < max_iters; ++it) {
+        cudaGraphConditionalHandle dummy = 0;
+        HDGB_CUDA(enqueue_iteration(c, variant, prec, dummy, 0));
+        HDGB_CUDA(cudaMemcpyAsync(h, c->d_st, sizeof(CGState), cudaMemcpyDeviceToHost, c->s));
+        HDGB_CUDA(cudaStreamSynchronize(c->s));
+        if (getenv("HDGB_DEBUG"))
+          fprintf(stderr, "it=%d rho=%.6e pw=%.6e alpha=%.6e beta=%.6e rr=%.6e rz=%.6e rn=%.6e thr=%.3e done=%d\n",
+                  h->it, h->rho, h->pw, h->alpha, h->beta, h->rr, h->rz, h->rn, h->thr, h->done);
+        if (h->done) break;
+      }
+    }
+    HDGB_CUDA(cudaMemcpyAsync(h, c->d_st, sizeof(CGState), cudaMemcpyDeviceToHost, c->s));
+    HDGB_CUDA(cudaStreamSynchronize(c->s));
+    if (use_graph) c->launches += 4LL * (h->it > 0 ? h->it - 1 : 0);
+  }
+  HDGB_CUDA(cudaMemcpyAsync(x, v + V_X * n, bytes, cudaMemcpyDeviceToDevice, c->s));
+  HDGB_CUDA(cudaEventRecord(c->ev_out, c->s));
+  HDGB_CUDA(cudaStreamWaitEvent(us, c->ev_out, 0));
+  *iters = h->it;
+  *relres = h->relres;
+  *converged = h->converged;
+  if (h->status == HDGB_EBREAKDOWN) {
+    set_error("conjugate gradient breakdown: non-positive curvature");
+    return HDGB_EBREAKDOWN;
+  }
+  if (h->status == HDGB_ENONFINITE) {
+    set_error("non-finite residual during iteration");
+    return HDGB_ENONFINITE;
+  }
+  return HDGB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,191 @@
+// Internal definitions shared by the hdgb CUDA translation units.
+//
+// Device data layout (HBM): one all-face FP64 vector per field in the reference
+// pack_all order (hdgbox/mesh.py:215-249, 324-326).  Face ids are global over the
+// three directions: fid = foff[d] + f with foff = (0, nf0, nf0+nf1).  A face block
+// holds N*N doubles [t1][t2], t2 fastest.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/hdgb.h"
+
+#define HDGB_MAX_N 17
+#define HDGB_NT 256            // threads per CTA of the element / face kernels
+#define HDGB_RED_BLOCKS 592    // fixed grid (4 x 148 SMs) of the reduction kernels
+
+namespace hdgb {
+
+enum { MODE_APPLY = 0, MODE_CG = 1 };
+
+// Mesh geometry in closed form (replaces the int64 index arrays of mesh.py:105-137).
+struct Geo {
+  int n1, n2, n3;
+  int64_t ne;
+  int64_t nf[3];
+  int64_t foff[3];
+  int kind[6];  // side kinds x1lo,x1hi,x2lo,x2hi,x3lo,x3hi
+};
+
+__host__ __device__ inline int64_t face_lo(const Geo& g, int d, int i, int j, int k) {
+  if (d == 0) return i + (int64_t)(g.n1 + 1) * (j + (int64_t)g.n2 * k);
+  if (d == 1) return i + (int64_t)g.n1 * (j + (int64_t)(g.n2 + 1) * k);
+  return i + (int64_t)g.n1 * (j + (int64_t)g.n2 * k);
+}
+__host__ __device__ inline int64_t face_step(const Geo& g, int d) {
+  return d == 0 ? 1 : (d == 1 ? (int64_t)g.n1 : (int64_t)g.n1 * g.n2);
+}
+// plane index (0..n_d) and the two tangential element coordinates of face f (dir d)
+__host__ __device__ inline void face_coords(const Geo& g, int d, int64_t f, int& plane, int& t1, int& t2) {
+  if (d == 0) {
+    plane = (int)(f % (g.n1 + 1));
+    int64_t q = f / (g.n1 + 1);
+    t1 = (int)(q % g.n2);
+    t2 = (int)(q / g.n2);
+  } else if (d == 1) {
+    t1 = (int)(f % g.n1);
+    int64_t q = f / g.n1;
+    plane = (int)(q % (g.n2 + 1));
+    t2 = (int)(q / (g.n2 + 1));
+  } else {
+    t1 = (int)(f % g.n1);
+    int64_t q = f / g.n1;
+    t2 = (int)(q % g.n2);
+    plane = (int)(q / g.n2);
+  }
+}
+__host__ __device__ inline int nd_of(const Geo& g, int d) { return d == 0 ? g.n1 : (d == 1 ? g.n2 : g.n3); }
+// kind of a face on plane `plane` of direction d (mesh.py:129-136)
+__host__ __device__ inline int face_kind(const Geo& g, int d, int plane) {
+  if (plane == 0) return g.kind[2 * d];
+  if (plane == nd_of(g, d)) return g.kind[2 * d + 1];
+  return HDGB_INTERIOR;
+}
+// uniform-mesh face class for face-wise tables: 0 both sides, 1 low boundary (B side only), 2 high boundary
+__host__ __device__ inline int face_class(const Geo& g, int d, int plane) {
+  int k = face_kind(g, d, plane);
+  if (k == HDGB_DIRICHLET || k == HDGB_NEUMANN) return plane == 0 ? 1 : 2;
+  return 0;  // interior or slab interface (tables include both elements)
+}
+__host__ __device__ inline bool kind_unknown(int k) { return k != HDGB_DIRICHLET; }
+__host__ __device__ inline bool kind_counts(int k) { return k != HDGB_DIRICHLET && k != HDGB_HALO_PEER; }
+
+// Small constant tables, one contiguous device block (offsets in doubles).
+struct TabOff {
+  int BS, T, MS, S, St, w, Lam, gcc, total;
+  __host__ __device__ void set(int N) {
+    BS = 0;
+    T = BS + 2 * N;
+    MS = T + N * N;
+    S = MS + N * N;
+    St = S + N * N;
+    w = St + N * N;
+    Lam = w + N;
+    gcc = Lam + N;
+    total = gcc + 2;
+  }
+};
+
+// PCG device state (solver.py:282-321 scalars), lives in device memory.
+struct CGState {
+  double rho, alpha, beta, norm0, thr, rn, pw, rr, rz, relres, rtol, atol;
+  int32_t it, max_iters, done, status, converged, pad;
+  uint32_t cnt[4];  // last-CTA tickets of the reduction kernels
+};
+
+struct OpArgs {
+  Geo g;
+  const double* u;
+  double* r;
+  double* xbuf;
+  int64_t xstride;
+  uint32_t* tickets;
+  double* facedot;
+  const double* tab;
+  const double* dz;      // N^3 shared table (uniform) or nullptr
+  const double* widths;  // n1+n2+n3 per-axis widths
+  double lam;
+  double al_u[4];        // uniform alpha0..alpha3
+  int uniform;
+  const CGState* st;     // CG mode: early-exit flag
+};
+
+struct FaceArgs {
+  Geo g;
+  int64_t nfaces;        // total faces
+  const double* tab;
+  const double* ycls;    // [3][3][N*N] class tables (uniform) or nullptr
+  const double* yfull;   // all-face table (non-uniform) or nullptr
+  int prec;
+  // apply: z = P in
+  const double* in;
+  double* out;
+  // generic transform
+  const double* A;       // device N*N (transform kernel)
+  // CG fused update
+  double* x;
+  double* p;
+  double* r;
+  const double* w;
+  double* z;
+  double* part;          // per-CTA partials [gridDim][2]
+  CGState* st;
+};
+
+}  // namespace hdgb
+
+struct hdgb_ctx {
+  int dev;
+  int N, p;
+  hdgb::Geo g;
+  double lam;
+  int uniform;
+  double al_u[4];
+  int64_t n_all, n_unknown, nfaces;
+  int64_t xstride;
+  double* d_tab = nullptr;
+  double* d_dz = nullptr;
+  double* d_widths = nullptr;
+  double* d_yinv_cls = nullptr;   // block/eigen: 1/y      [3][3][N2]
+  double* d_y_cls = nullptr;      // eigen diagonal y      [3][3][N2]
+  double* d_dn_cls = nullptr;     // nodal diagonal        [3][3][N2]
+  double* d_yinv_full = nullptr;  // non-uniform variants (n_all each)
+  double* d_y_full = nullptr;
+  double* d_dn_full = nullptr;
+  double* d_xbuf = nullptr;
+  uint32_t* d_tickets = nullptr;
+  double* d_facedot = nullptr;
+  double* d_part = nullptr;
+  double* d_A = nullptr;          // transform matrix scratch N*N
+  hdgb::CGState* d_st = nullptr;
+  hdgb::CGState* h_st = nullptr;  // pinned mirror
+  double* d_vec = nullptr;        // CG vectors x r z p w F (6 * n_all)
+  double* d_io = nullptr;         // host-path staging (2 * n_all)
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaGraphExec_t graph[2][4] = {{nullptr}};
+  int graph_iters = 0;
+  int64_t launches = 0;
+  int smem_op = 0;
+};
+
+namespace hdgb {
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+// launchers (defined per translation unit)
+cudaError_t launch_op(hdgb_ctx* c, int variant, int mode, const double* u, double* r, cudaStream_t s);
+cudaError_t launch_face_transform(hdgb_ctx* c, const double* A_dev, const double* in, double* out, cudaStream_t s);
+cudaError_t launch_prec(hdgb_ctx* c, int kind, const double* in, double* out, cudaStream_t s);
+cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s);
+cudaError_t launch_build_tables(hdgb_ctx* c, cudaStream_t s);
+cudaError_t op_set_smem_limits(hdgb_ctx* c);
+}  // namespace hdgb
+
+#define HDGB_CUDA(call)                                 \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return hdgb::cuda_fail(_e, #call); \
+  } while (0)

@@ -38,3 +38,11 @@ def relerr(a, b):
     b = np.asarray(b)
     scale = max(float(np.max(np.abs(b))) if b.size else 0.0, 1e-300)
     return float(np.max(np.abs(a - b))) / scale if a.size else 0.0
+
+
+def sinsin_field(mesh, basis, lam):
+    """Element-nodal f for u = sin(pi x) sin(pi y) sin(pi z): f = (lam + 3 pi^2) u."""
+    X1, X2, X3 = mesh.element_node_grids(basis.nodes)
+    pi = np.pi
+    val = (lam + 3 * pi * pi) * np.sin(pi * X1) * np.sin(pi * X2) * np.sin(pi * X3)
+    return np.broadcast_to(val, (mesh.n_elements,) + (basis.n,) * 3).copy()
