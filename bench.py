@@ -1,0 +1,399 @@
+"""Benchmark of the LDG-H trace-operator hot path (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--sweep]
+
+Workload (BASELINE configs[1]): unit cube, 16^3 uniform elements, p = 8 (GLL),
+lambda = 1, homogeneous Dirichlet, tau = 25 ("element" convention).  A step is
+one plain (Alg. 2) operator apply r = K u over all faces of a seeded
+uniform[-1,1] trace vector resident in HBM; the 8.5 MB vectors fit in L2, so
+L2 is flushed (a 512 MB write) before every timed step and only the apply is
+inside the CUDA events.  `value` = trace unknowns / apply time (trace-DOF/s).
+`e2e` times the same apply through the C ABI with pinned HOST buffers
+(hdgb_op_apply_host: H2D + kernel + D2H).  The line also carries the fused
+block-PCG solve of the same config (CG us per unknown per iteration), the
+transformed (Alg. 3) apply, the roofline of the operator kernel, and the CPU
+oracle timed on this host.
+
+Multi-GPU (torchrun, N > 1): weak scaling, each rank owns a 16^3 slab of a
+[0,N]x[0,1]^2 box (x-slab partition); the apply adds the NCCL halo exchange of
+the interface x-face planes.  `--impl reference` times the CPU oracle port of
+the reference path on rank 0 only.
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = dict(n_el=(16, 16, 16), p=8, lam=1.0, tau=25.0)
+L2_FLUSH_BYTES = 512 << 20
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _traffic_record():
+    try:
+        with open(os.path.join(ROOT, "profiles", "op_traffic.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons through NVML while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, device=0):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def record(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def build_problem(rank=0, world=1):
+    import paper_2007_11891_b200 as hb
+
+    n1, n2, n3 = CFG["n_el"]
+    mesh = hb.Mesh((n1 * world, n2, n3), (0, 0, 0), (float(world), 1.0, 1.0), "dirichlet")
+    cfg = hb.SolverConfig(lam=CFG["lam"], tau=CFG["tau"])
+    ctx = hb.make_context(mesh, CFG["p"], cfg)
+    return hb, mesh, cfg, ctx
+
+
+def _sin_rhs(hb, mesh, ctx):
+    X1, X2, X3 = mesh.element_node_grids(ctx.basis.nodes)
+    pi = math.pi
+    f = (CFG["lam"] + 3 * pi * pi) * np.sin(pi * X1) * np.sin(pi * X2) * np.sin(pi * X3)
+    f = np.broadcast_to(f, (mesh.n_elements,) + (ctx.basis.n,) * 3).copy()
+    return hb.pack_unknowns(hb.build_rhs(f, None, None, ctx))
+
+
+def cpu_oracle_apply(seconds=10.0, threads=1, steps=None, warmup=1):
+    """Time the CPU oracle (numpy restatement of the reference apply) on config 2."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import hdg_oracle as O
+
+    octx = O.problem(CFG["n_el"], CFG["p"], CFG["lam"], tau=CFG["tau"])
+    grid, n = octx["grid"], octx["n"]
+    N = grid.n_unknowns(n)
+    v = np.random.default_rng(1).uniform(-1.0, 1.0, N)
+    times = []
+    with threadpool_limits(limits=threads):
+        for _ in range(max(warmup, 0)):
+            O.apply_op_packed(octx, v)
+        t_start = time.perf_counter()
+        while True:
+            t0 = time.perf_counter()
+            O.apply_op_packed(octx, v)
+            times.append(time.perf_counter() - t0)
+            if steps is not None:
+                if len(times) >= steps:
+                    break
+            elif time.perf_counter() - t_start >= seconds and len(times) >= 3:
+                break
+    return N, times
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    N, times = cpu_oracle_apply(threads=cores, steps=args.steps, warmup=args.warmup)
+    t = statistics.median(times)
+    val = N / t
+    line = {
+        "metric": "FP64 trace-DOF/s per operator apply (plain Alg. 2, hdg_op_3d)",
+        "value": val, "unit": "trace-DOF/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1] trace vector)",
+        "config": {"workload": "BASELINE configs[1]: 16^3 elements, p=8, lambda=1, unit cube, Dirichlet",
+                   "trace_unknowns": N},
+        "cpu_baseline": {"value": val, "unit": "trace-DOF/s", "cores": cores, "kind": "port",
+                         "sample": f"{len(times)} oracle applies of config 2 (numpy restatement of "
+                                   f"hdgbox hdg_op_3d; BLAS threads={cores})"},
+        "e2e": {"value": val, "unit": "trace-DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def _timed_apply(dc, u, r, variant, steps, warmup, flush, stream):
+    import torch
+
+    for _ in range(warmup):
+        flush.zero_()
+        dc.apply(u, variant, out=r)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    l0 = dc.launches()
+    for a, b in evs:
+        flush.zero_()
+        a.record(stream)
+        dc.apply(u, variant, out=r)
+        b.record(stream)
+    torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in evs]
+    return ms, dc.launches() - l0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p, n = CFG["p"], CFG["p"] + 1
+    if world > 1:
+        import paper_2007_11891_b200 as hb
+        from paper_2007_11891_b200.distributed import slab_mesh, slab_side_kinds
+
+        n1, n2, n3 = CFG["n_el"]
+        gn = (n1 * world, n2, n3)
+        mesh = slab_mesh(gn, (0.0, 0.0, 0.0), (float(world), 1.0, 1.0), rank, world)
+        cfg = hb.SolverConfig(lam=CFG["lam"], tau=CFG["tau"])
+        ctx = hb.make_context(mesh, p, cfg)
+        ctx._hdgb_device = hb.DeviceContext(ctx.basis, mesh, CFG["lam"], device=local,
+                                            side_kinds=slab_side_kinds(rank, world))
+        N_global = hb.Mesh(gn, (0, 0, 0), (float(world), 1.0, 1.0)).n_trace_unknowns(p)
+    else:
+        hb, mesh, cfg, ctx = build_problem()
+        N_global = mesh.n_trace_unknowns(p)
+    dc = hb.device_context(ctx)
+    N = mesh.n_trace_unknowns(p) if world == 1 else N_global // world
+    N_all = mesh.n_all(p)
+    v = np.random.default_rng(1 + rank).uniform(-1.0, 1.0, dc.n_unknown)
+    u = dc.unpack(torch.from_numpy(v).cuda())
+    r = dc.empty()
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    halo = None
+    if world > 1:
+        from paper_2007_11891_b200.distributed import SlabHalo
+
+        halo = SlabHalo(dc, rank, world)
+
+    def apply_step(variant):
+        dc.apply(u, variant, out=r)
+        if halo is not None:
+            halo.exchange_add(r)
+
+    # ---- device-resident operator apply (value + roofline)
+    steps, warm = args.steps, max(args.warmup, 3)
+    with ClockSampler(local) as clk:
+        for _ in range(warm):
+            flush.zero_()
+            apply_step(0)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        l0 = dc.launches()
+        for a, b in evs:
+            flush.zero_()
+            a.record(stream)
+            apply_step(0)
+            b.record(stream)
+        torch.cuda.synchronize()
+        launches = dc.launches() - l0
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in evs]
+    t_step = statistics.fmean(ms) * 1e-3
+    if world > 1:
+        tt = torch.tensor([t_step], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step = float(tt.item())
+    value = world * N / t_step
+
+    # ---- operator kernel alone (roofline): same launches, kernel-only events
+    ms_k, _ = _timed_apply(dc, u, r, 0, steps, 2, flush, stream)
+    t_k = statistics.fmean(ms_k) * 1e-3
+    ms_t, _ = _timed_apply(dc, u, r, 1, steps, 2, flush, stream)
+    t_tr = statistics.fmean(ms_t) * 1e-3
+    hbm, peak_kind = _peaks()
+    alg_bytes = 16 * N_all  # read u once + write r once, all faces (16 B per trace unknown)
+    achieved = alg_bytes / t_k / 1e9
+    traffic = _traffic_record()
+
+    # ---- e2e through the C ABI with pinned host buffers
+    h_u = torch.empty(N_all, dtype=torch.float64).pin_memory()
+    h_r = torch.empty(N_all, dtype=torch.float64).pin_memory()
+    h_u.copy_(u.cpu())
+    hu, hr = h_u.numpy(), h_r.numpy()
+    def e2e_step():
+        if world == 1:
+            dc.apply_host(hu, hr, 0)  # C ABI: H2D + kernel + D2H + sync
+        else:
+            ud = h_u.to("cuda", non_blocking=True)
+            dc.apply(ud, 0, out=r)
+            halo.exchange_add(r)
+            h_r.copy_(r, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+    for _ in range(2):
+        e2e_step()
+    e2e_ms = []
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        e2e_step()
+        b.record(stream)
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    t_e2e = statistics.median(e2e_ms) * 1e-3
+    apply_step(0)
+    assert np.array_equal(hr, r.cpu().numpy()), "e2e result differs from the device-resident apply"
+
+    # ---- fused block-PCG solve (CG us per unknown per iteration)
+    cg = None
+    if world == 1:
+        F = _sin_rhs(hb, mesh, ctx)
+        Fd = dc.unpack(torch.from_numpy(F).cuda())
+        x = torch.zeros_like(Fd)
+        for _ in range(2):
+            x.zero_()
+            it, rel, conv = dc.pcg(0, 1, Fd, x, 1e-10, 0.0, 10000)
+        cg_ms = []
+        for _ in range(5):
+            flush.zero_()
+            x.zero_()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            it, rel, conv = dc.pcg(0, 1, Fd, x, 1e-10, 0.0, 10000)
+            b.record(stream)
+            b.synchronize()
+            cg_ms.append(a.elapsed_time(b))
+        t_cg = statistics.median(cg_ms) * 1e-3
+        cg = {"preconditioner": "block (Alg. 4)", "iterations": it, "converged": conv, "relres": rel,
+              "solve_ms": t_cg * 1e3, "us_per_unknown_per_iter": t_cg / it / N * 1e6,
+              "ms_per_iter": t_cg / it * 1e3,
+              "hbm_frac_of_96B_per_unknown": (96 * N_all / (t_cg / it) / 1e9) / hbm,
+              "note": "whole solve incl. setup kernels, one CUDA graph with device-side while loop; "
+                      "config-2 vectors are L2-resident during the solve"}
+
+    # ---- CPU oracle on this host (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        Nc, times = cpu_oracle_apply(seconds=args.cpu_seconds, threads=1)
+        tc = statistics.median(times)
+        cpu = {"value": Nc / tc, "unit": "trace-DOF/s", "cores": 1, "kind": "port",
+               "sample": f"{len(times)} applies of config 2 by the numpy oracle (restatement of hdgbox "
+                         f"hdg_op_3d), threadpool_limits(1), median {tc * 1e3:.1f} ms; host "
+                         f"{os.cpu_count()} cores"}
+
+    line = {
+        "metric": "FP64 trace-DOF/s per operator apply (plain Alg. 2, hdg_op_3d)",
+        "value": value, "unit": "trace-DOF/s", "n_gpus": world, "steps": steps, "warmup": warm,
+        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded uniform[-1,1] trace vector; manufactured sin RHS for CG)",
+        "config": {"workload": "BASELINE configs[1]: 16^3 elements per GPU, p=8, lambda=1, unit cube per GPU, "
+                               "Dirichlet, tau=25 (element)",
+                   "trace_unknowns_per_gpu": N, "all_face_dofs_per_gpu": N_all,
+                   "l2": "flushed before every timed step (512 MB write)", "parallelism": f"x-slab dp{world}"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": (traffic or {}).get("bytes_per_launch"),
+                     "kernel": "op_kernel<9,plain,apply>", "kernel_ms": t_k * 1e3,
+                     "algorithmic_bytes_per_launch": alg_bytes, "peak_kind": peak_kind},
+        "transformed_apply": {"value": N / t_tr, "unit": "trace-DOF/s", "kernel_ms": t_tr * 1e3,
+                              "hbm_frac": (alg_bytes / t_tr / 1e9) / hbm},
+        "cg": cg,
+        "cpu_baseline": cpu,
+        "e2e": {"value": world * N / t_e2e, "unit": "trace-DOF/s", "h2d_bytes_per_step": 8 * N_all,
+                "d2h_bytes_per_step": 8 * N_all, "ms_per_step": t_e2e * 1e3,
+                "path": "hdgb_op_apply_host (C ABI, pinned host buffers)"},
+        "gpu_launches": launches,
+        "clocks": clk.record(),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

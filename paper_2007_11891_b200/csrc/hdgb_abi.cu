@@ -55,6 +55,7 @@ static void free_ctx(hdgb_ctx* c) {
   for (double* b : bufs)
     if (b) cudaFree(b);
   if (c->d_tickets) cudaFree(c->d_tickets);
+  if (c->d_finfo) cudaFree(c->d_finfo);
   if (c->d_st) cudaFree(c->d_st);
   if (c->h_st) cudaFreeHost(c->h_st);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
@@ -79,6 +80,7 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
 
   hdgb_ctx* c = new hdgb_ctx();
   c->dev = d->device;
+  if (const char* sb = getenv("HDGB_SLAB_MB")) c->slab_bytes = (int64_t)atof(sb) * (1LL << 20);
   if (cudaSetDevice(c->dev) != cudaSuccess) {
     delete c;
     return einval("invalid CUDA device");
@@ -186,6 +188,18 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
   CK(cudaMalloc(&c->d_xbuf, sizeof(double) * c->xstride * c->nfaces));
   CK(cudaMalloc(&c->d_tickets, sizeof(uint32_t) * c->nfaces));
   CK(cudaMemset(c->d_tickets, 0, sizeof(uint32_t) * c->nfaces));
+  {
+    // one byte per face: kind | (d*3 + class) << 3 (mesh.py:129-137 classification)
+    std::vector<uint8_t> finfo(c->nfaces);
+    for (int q = 0; q < 3; ++q)
+      for (int64_t f = 0; f < g.nf[q]; ++f) {
+        int plane, t1, t2;
+        face_coords(g, q, f, plane, t1, t2);
+        finfo[g.foff[q] + f] = (uint8_t)(face_kind(g, q, plane) | ((q * 3 + face_class(g, q, plane)) << 3));
+      }
+    CK(cudaMalloc(&c->d_finfo, c->nfaces));
+    CK(cudaMemcpy(c->d_finfo, finfo.data(), c->nfaces, cudaMemcpyHostToDevice));
+  }
   CK(cudaMalloc(&c->d_facedot, sizeof(double) * c->nfaces));
   CK(cudaMalloc(&c->d_part, sizeof(double) * 4 * HDGB_RED_BLOCKS + 64));
   CK(cudaMalloc(&c->d_A, sizeof(double) * N2));

@@ -3,283 +3,247 @@
 // preconditioner table builds (preconditioner.py:36-68, 178-204) and the
 // deterministic fixed-grid reductions.
 //
-// All face kernels run a persistent grid-stride loop over batches of FPC faces with a
-// FIXED grid size, so every per-CTA partial sum covers a fixed set of faces and the
-// final fixed-order reduction by the last CTA is bitwise reproducible.
+//  * pointwise kernels (no / diagonal preconditioner, the x/r updates): 4-way unrolled
+//    grid-stride streams with all loads issued before use; per-face kind/class comes from
+//    a one-byte-per-face table, so the hot loop has no index arithmetic beyond i / N^2
+//  * block kernels (Alg. 4 z = (S(x)S) y^-1 (S^T(x)S^T) r, and generic (A(x)A)): batches
+//    of faces staged with cp.async (double-buffered), transforms as row passes (one face
+//    row per thread in registers, the 1D matrix a shared-memory broadcast)
+//  * every reduction runs on a FIXED grid and finishes in the last CTA in fixed order, so
+//    dot products are bitwise reproducible run to run.
 #include <cmath>
 
 #include "hdgb_internal.cuh"
 
 namespace hdgb {
 
-enum { FK_PREC = 0, FK_TRANSFORM = 1, FK_CG_INIT = 2, FK_CG_UPDATE = 3 };
-
-template <int N>
-struct FaceCfg {
-  static constexpr int N2 = N * N;
-  static constexpr int FPC = (N2 >= HDGB_NT) ? 1 : (HDGB_NT / N2);
-  static constexpr int P = (N % 2 == 0) ? N + 1 : N;
-  static constexpr int smem_doubles() { return 2 * N * P + N + 3 * FPC * N2; }
-};
-
-// ---------------------------------------------------------------- reductions
-// Deterministic block sum of two values (fixed tree); result valid in thread 0.
-__device__ __forceinline__ void block_sum2(double& a, double& b) {
-  __shared__ double ra[HDGB_NT / 32], rb[HDGB_NT / 32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
-  }
-  __syncthreads();
-  if (lane == 0) {
-    ra[w] = a;
-    rb[w] = b;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double sa = 0.0, sb = 0.0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
-      sa += ra[q];
-      sb += rb[q];
-    }
-    a = sa;
-    b = sb;
-  }
+int grid_for(int64_t work, int per) {
+  int64_t b = (work + per - 1) / per;
+  if (b > 148 * 8) b = 148 * 8;
+  return (int)(b < 1 ? 1 : b);
 }
 
-// Publish this CTA's partials, return true in the CTA that arrives last.
-__device__ bool publish_last(double* part, double a, double b, uint32_t* cnt) {
-  __shared__ bool am_last;
-  if (threadIdx.x == 0) {
-    part[2 * blockIdx.x] = a;
-    part[2 * blockIdx.x + 1] = b;
-    __threadfence();
-    unsigned t = atomicInc(cnt, gridDim.x - 1);
-    am_last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (am_last) __threadfence();
-  return am_last;
+__device__ __forceinline__ void cp_async8f(double* smem_dst, const double* gsrc) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
 }
 
-// Fixed-order sum of all CTA partials (run by the last CTA).
-__device__ void final_sum2(const double* part, int nb, double& a, double& b) {
-  double sa = 0.0, sb = 0.0;
-  for (int q = threadIdx.x; q < nb; q += blockDim.x) {
-    sa += __ldcg(part + 2 * q);
-    sb += __ldcg(part + 2 * q + 1);
-  }
-  block_sum2(sa, sb);
-  a = sa;
-  b = sb;
-}
+// ================================================================ pointwise kernels
+enum { PW_PREC = 0, PW_INIT = 1, PW_UPDATE = 2 };
+constexpr int PW_U = 4;       // elements per thread per sweep
+constexpr int PW_GRID = 1184; // fixed grid (8 CTAs x 148 SMs)
 
-// ---------------------------------------------------------------- face kernel
-template <int N, int PREC, int FK>
-__global__ void __launch_bounds__(HDGB_NT) face_kernel(FaceArgs a) {
-  using C = FaceCfg<N>;
-  constexpr int N2 = C::N2, FPC = C::FPC, P = C::P;
-  if ((FK == FK_CG_INIT || FK == FK_CG_UPDATE) && a.st->done) return;
-
-  extern __shared__ double smem[];
-  double* sA = smem;            // forward matrix [i][j] pitch P  (S^T, or A)
-  double* sB = sA + N * P;      // backward matrix (S)
-  double* sW = sB + N * P;      // weights (unused placeholder for alignment)
-  double* s0 = sW + N;          // FPC x N2
-  double* s1 = s0 + FPC * N2;
-  double* s2 = s1 + FPC * N2;
-  __shared__ unsigned char sKind[FPC];
-  __shared__ int sCls[FPC];
-
-  const Geo& g = a.g;
-  const int tid = threadIdx.x;
-  TabOff to;
-  to.set(N);
-  if (FK == FK_TRANSFORM) {
-    for (int t = tid; t < N2; t += blockDim.x) sA[(t / N) * P + t % N] = a.A[t];
-  } else if (PREC == HDGB_PREC_BLOCK) {
-    for (int t = tid; t < N2; t += blockDim.x) {
-      sA[(t / N) * P + t % N] = a.tab[to.St + t];
-      sB[(t / N) * P + t % N] = a.tab[to.S + t];
-    }
-  }
-  __syncthreads();
-
-  double acc_rr = 0.0, acc_rz = 0.0;
-  const double alpha = (FK == FK_CG_UPDATE) ? a.st->alpha : 0.0;
-  const int64_t nb = (a.nfaces + FPC - 1) / FPC;
-
-  for (int64_t bt = blockIdx.x; bt < nb; bt += gridDim.x) {
-    const int64_t f0 = bt * FPC;
-    const int nf = (int)min((int64_t)FPC, a.nfaces - f0);
-    if (tid < nf) {
-      int64_t fid = f0 + tid;
-      int d = fid >= g.foff[2] ? 2 : (fid >= g.foff[1] ? 1 : 0);
-      int plane, t1, t2;
-      face_coords(g, d, fid - g.foff[d], plane, t1, t2);
-      int k = face_kind(g, d, plane);
-      sKind[tid] = (unsigned char)k;
-      sCls[tid] = d * 3 + face_class(g, d, plane);
-    }
-    __syncthreads();
-    // load (+ fused vector update)
-    for (int it = tid; it < nf * N2; it += blockDim.x) {
-      const int64_t gi = f0 * N2 + it;
-      double v;
-      if (FK == FK_PREC || FK == FK_TRANSFORM) {
-        v = a.in[gi];
-      } else if (FK == FK_CG_INIT) {
-        v = (sKind[it / N2] == HDGB_DIRICHLET) ? 0.0 : a.in[gi] - a.w[gi];  // r = F - K x
-        a.r[gi] = v;
-      } else {
-        double xv = a.x[gi], pv = a.p[gi], rv = a.r[gi], wv = a.w[gi];
-        xv += alpha * pv;  // x += alpha p
-        rv -= alpha * wv;  // r -= alpha w
-        a.x[gi] = xv;
-        a.r[gi] = rv;
-        v = rv;
-      }
-      s0[it] = v;
-    }
-    __syncthreads();
-    const double* zres = s0;
-    if (FK == FK_TRANSFORM || PREC == HDGB_PREC_BLOCK) {
-      // s1 = (A (x) A) s0: contract t2 then t1
-      for (int it = tid; it < nf * N2; it += blockDim.x) {
-        int f = it / N2, rem = it - f * N2, i = rem / N, j = rem - i * N;
-        const double* x = s0 + f * N2 + i * N;
-        double s = 0.0;
+template <int N, int PREC, int FK, bool WITHZ>
+__global__ void __launch_bounds__(256) pw_kernel(FaceArgs a, const uint8_t* __restrict__ finfo, unsigned n) {
+  constexpr unsigned N2 = N * N;
+  if (FK != PW_PREC && a.st->done) return;
+  const double alpha = FK == PW_UPDATE ? a.st->alpha : 0.0;
+  double rr = 0.0, rz = 0.0;
+  const unsigned stride = gridDim.x * 256u * PW_U;
+  for (unsigned base = blockIdx.x * 256u * PW_U + threadIdx.x; base < n; base += stride) {
+    double v0[PW_U], v1[PW_U], v2[PW_U], v3[PW_U];
+    uint8_t inf[PW_U];
 #pragma unroll
-        for (int b = 0; b < N; ++b) s = fma(sA[j * P + b], x[b], s);
-        s1[it] = s;
-      }
-      __syncthreads();
-      for (int it = tid; it < nf * N2; it += blockDim.x) {
-        int f = it / N2, rem = it - f * N2, i = rem / N, j = rem - i * N;
-        const double* x = s1 + f * N2 + j;
-        double s = 0.0;
-#pragma unroll
-        for (int b = 0; b < N; ++b) s = fma(sA[i * P + b], x[b * N], s);
-        if (FK != FK_TRANSFORM) {
-          // * y^-1 (BlockPreconditioner, preconditioner.py:100-104)
-          int64_t gi = f0 * N2 + it;
-          double yi = a.ycls ? __ldg(a.ycls + sCls[f] * N2 + rem) : __ldg(a.yfull + gi);
-          s *= yi;
-        }
-        s2[it] = s;
-      }
-      __syncthreads();
-      zres = s2;
-      if (FK != FK_TRANSFORM) {
-        for (int it = tid; it < nf * N2; it += blockDim.x) {
-          int f = it / N2, rem = it - f * N2, i = rem / N, j = rem - i * N;
-          const double* x = s2 + f * N2 + i * N;
-          double s = 0.0;
-#pragma unroll
-          for (int b = 0; b < N; ++b) s = fma(sB[j * P + b], x[b], s);
-          s1[it] = s;
-        }
-        __syncthreads();
-        for (int it = tid; it < nf * N2; it += blockDim.x) {
-          int f = it / N2, rem = it - f * N2, i = rem / N, j = rem - i * N;
-          const double* x = s1 + f * N2 + j;
-          double s = 0.0;
-#pragma unroll
-          for (int b = 0; b < N; ++b) s = fma(sB[i * P + b], x[b * N], s);
-          s2[it] = s;
-        }
-        __syncthreads();
-      }
-    }
-    // store z (Dirichlet faces zero) + dot partials
-    for (int it = tid; it < nf * N2; it += blockDim.x) {
-      const int f = it / N2;
-      const int64_t gi = f0 * N2 + it;
-      const int k = sKind[f];
-      double z;
-      if (FK == FK_TRANSFORM) {
-        z = zres[it];
-      } else {
-        const double v = s0[it];
-        if (k == HDGB_DIRICHLET) {
-          z = 0.0;
-        } else if (PREC == HDGB_PREC_BLOCK) {
-          z = zres[it];
-        } else if (PREC == HDGB_PREC_DIAG_NODAL || PREC == HDGB_PREC_DIAG_EIGEN) {
-          int rem = it - f * N2;
-          double dg = a.ycls ? __ldg(a.ycls + sCls[f] * N2 + rem) : __ldg(a.yfull + gi);
-          z = v / dg;  // DiagonalPreconditioner divides (preconditioner.py:158, 165)
+    for (int k = 0; k < PW_U; ++k) {  // issue every load first
+      const unsigned i = base + k * 256u;
+      if (i < n) {
+        inf[k] = __ldg(finfo + i / N2);
+        if (FK == PW_PREC) {
+          v0[k] = a.in[i];
+        } else if (FK == PW_INIT) {
+          v0[k] = a.in[i];
+          v1[k] = a.w[i];
         } else {
-          z = v;
-        }
-        if (FK == FK_CG_INIT || FK == FK_CG_UPDATE) {
-          if (kind_counts(k)) {
-            acc_rr = fma(v, v, acc_rr);
-            acc_rz = fma(v, z, acc_rz);
-          }
-          if (FK == FK_CG_INIT) a.p[gi] = z;
+          v0[k] = a.x[i];
+          v1[k] = a.p[i];
+          v2[k] = a.r[i];
+          v3[k] = a.w[i];
         }
       }
-      a.out[gi] = z;
     }
-    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < PW_U; ++k) {
+      const unsigned i = base + k * 256u;
+      if (i >= n) continue;
+      const int kind = finfo_kind(inf[k]);
+      double val;
+      if (FK == PW_PREC) {
+        val = v0[k];
+      } else if (FK == PW_INIT) {
+        val = kind == HDGB_DIRICHLET ? 0.0 : v0[k] - v1[k];  // r = F - K x0 (solver.py:291)
+        a.r[i] = val;
+      } else {
+        double xv = v0[k], rv = v2[k];
+        xv += alpha * v1[k];  // x += alpha p  (solver.py:313)
+        rv -= alpha * v3[k];  // r -= alpha w  (solver.py:314)
+        a.x[i] = xv;
+        a.r[i] = rv;
+        val = rv;
+      }
+      if (FK == PW_PREC || WITHZ) {
+        double z;
+        if (kind == HDGB_DIRICHLET) {
+          z = 0.0;
+        } else if (PREC == HDGB_PREC_NONE) {
+          z = val;
+        } else {  // DiagonalPreconditioner divides (preconditioner.py:158, 165)
+          const unsigned q = i - (i / N2) * N2;
+          const double dg = a.ycls ? __ldg(a.ycls + finfo_cls(inf[k]) * N2 + q) : __ldg(a.yfull + i);
+          z = val / dg;
+        }
+        a.out[i] = z;
+        if (FK == PW_INIT) a.p[i] = z;
+        if (FK != PW_PREC && kind_counts(kind)) rz = fma(val, z, rz);
+      }
+      if (FK != PW_PREC && kind_counts(kind)) rr = fma(val, val, rr);
+    }
   }
-
-  if (FK == FK_CG_INIT || FK == FK_CG_UPDATE) {
-    block_sum2(acc_rr, acc_rz);
-    if (publish_last(a.part, acc_rr, acc_rz, &a.st->cnt[FK == FK_CG_INIT ? 0 : 1])) {
-      double rr, rz;
-      final_sum2(a.part, gridDim.x, rr, rz);
+  if (FK != PW_PREC) {
+    block_sum2(rr, rz);
+    if (publish_last(a.part, rr, rz, &a.st->cnt[FK == PW_INIT ? 0 : 1])) {
+      double trr, trz;
+      final_sum2(a.part, gridDim.x, trr, trz);
       if (threadIdx.x == 0) {
         CGState* st = a.st;
-        const double rn = sqrt(rr);
-        st->rr = rr;
-        st->rz = rz;
-        if (FK == FK_CG_INIT) {
-          // solver.py:290-301
-          st->norm0 = rn;
-          st->rn = rn;
-          st->it = 0;
-          if (!isfinite(rn)) {
-            st->status = HDGB_ENONFINITE;
-            st->done = 1;
-          } else if (rn == 0.0 || rn <= st->atol) {
-            st->converged = 1;
-            st->done = 1;
-            st->relres = 0.0;
-          } else {
-            st->thr = fmax(st->rtol * rn, st->atol);
-            st->rho = rz;
-            st->relres = 1.0;
-          }
-        } else {
-          // solver.py:313-321
-          st->it += 1;
-          st->rn = rn;
-          if (!isfinite(rn)) {
-            st->status = HDGB_ENONFINITE;
-            st->done = 1;
-          } else if (rn <= st->thr) {
-            st->converged = 1;
-            st->done = 1;
-            st->relres = rn / st->norm0;
-          } else {
-            st->relres = rn / st->norm0;
-            if (st->it >= st->max_iters) {
-              st->done = 1;
-            } else {
-              st->beta = rz / st->rho;
-              st->rho = rz;
-            }
-          }
+        if (FK == PW_INIT) cg_init_r(st, trr);
+        else cg_update_r(st, trr);
+        if (WITHZ && !st->done) {
+          if (FK == PW_INIT) cg_init_z(st, trz);
+          else cg_update_z(st, trz);
         }
       }
     }
   }
 }
 
+// ================================================================ block / transform kernels
+enum { BK_PREC = 0, BK_INIT = 1, BK_UPDATE = 2, BK_TRANSFORM = 3 };
+
+template <int N>
+struct BlkCfg {
+  static constexpr int N2 = N * N;
+  static constexpr int FPC = (256 / N) > 0 ? (256 / N) : 1;  // faces per batch: rows per pass <= 256
+  static constexpr int V = FPC * N2;
+  static constexpr int TP = N + (N & 1);
+  static constexpr int smem_doubles() { return 2 * N * TP + 4 * V; }
+};
+
+// rows pass over nf faces of X: Y_f[j][r] = sum_b A[j][b] X_f[r][b], stored transposed via store
+template <int N, typename Store>
+__device__ __forceinline__ void rows_pass(const double* __restrict__ A, const double* __restrict__ X, int nf,
+                                          Store store) {
+  constexpr int N2 = N * N, TP = BlkCfg<N>::TP;
+  for (int it = threadIdx.x; it < nf * N; it += blockDim.x) {
+    const int f = it / N, r = it - f * N;
+    double x[N + 1];
+    const double* xr = X + f * N2 + r * N;
+#pragma unroll
+    for (int b = 0; b < N; ++b) x[b] = xr[b];
+    x[N] = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < N; ++j) {
+      const double* Aj = A + j * TP;
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int b = 0; b < N; b += 2) {
+        const double2 t = *reinterpret_cast<const double2*>(Aj + b);
+        s0 = fma(t.x, x[b], s0);
+        s1 = fma(t.y, x[b + 1], s1);
+      }
+      store(f, j, r, s0 + s1);
+    }
+  }
+}
+
+template <int N, int FK>
+__global__ void __launch_bounds__(256) blk_kernel(FaceArgs a, const uint8_t* __restrict__ finfo) {
+  using C = BlkCfg<N>;
+  constexpr int N2 = C::N2, FPC = C::FPC, V = C::V, TP = C::TP;
+  if ((FK == BK_INIT || FK == BK_UPDATE) && a.st->done) return;
+  extern __shared__ __align__(16) double smem[];
+  double* sA = smem;            // forward matrix [j][b] (S^T, or A)
+  double* sB = sA + N * TP;     // backward matrix (S)
+  double* sIn0 = sB + N * TP;   // 2 x V staged inputs
+  double* t1 = sIn0 + 2 * V;
+  double* t2 = t1 + V;
+  __shared__ uint8_t sInf[FPC];
+
+  TabOff to;
+  to.set(N);
+  for (int t = threadIdx.x; t < N * TP; t += blockDim.x) {
+    const int r = t / TP, c = t - r * TP;
+    if (FK == BK_TRANSFORM) {
+      sA[t] = c < N ? a.A[r * N + c] : 0.0;
+    } else {
+      sA[t] = c < N ? a.tab[to.St + r * N + c] : 0.0;  // S^T[r][c]
+      sB[t] = c < N ? a.tab[to.S + r * N + c] : 0.0;   // S[r][c]
+    }
+  }
+  const int64_t nb = (a.nfaces + FPC - 1) / FPC;
+  auto issue = [&](int64_t bt, double* dst) {
+    const int64_t f0 = bt * FPC;
+    const int nf = (int)min((int64_t)FPC, a.nfaces - f0);
+    const double* src = a.in + f0 * N2;
+    for (int it = threadIdx.x; it < nf * N2; it += blockDim.x) cp_async8f(dst + it, src + it);
+  };
+  int64_t bt = blockIdx.x;
+  if (bt < nb) issue(bt, sIn0);
+  asm volatile("cp.async.commit_group;\n" ::);
+  double rz = 0.0;
+  int buf = 0;
+  for (; bt < nb; bt += gridDim.x, buf ^= 1) {
+    double* sIn = sIn0 + buf * V;
+    if (bt + gridDim.x < nb) issue(bt + gridDim.x, sIn0 + (buf ^ 1) * V);
+    asm volatile("cp.async.commit_group;\n" ::);
+    const int64_t f0 = bt * FPC;
+    const int nf = (int)min((int64_t)FPC, a.nfaces - f0);
+    if (threadIdx.x < nf) sInf[threadIdx.x] = finfo[f0 + threadIdx.x];
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    __syncthreads();
+    // (A (x) A) X = A X A^T as two transposing row passes
+    rows_pass<N>(sA, sIn, nf, [&](int f, int j, int r, double v) { t1[f * N2 + j * N + r] = v; });
+    __syncthreads();
+    rows_pass<N>(sA, t1, nf, [&](int f, int j, int r, double v) {
+      const int q = j * N + r;
+      if (FK != BK_TRANSFORM) {  // * y^-1 (BlockPreconditioner, preconditioner.py:100-104)
+        v *= a.ycls ? __ldg(a.ycls + finfo_cls(sInf[f]) * N2 + q) : __ldg(a.yfull + (f0 + f) * N2 + q);
+      }
+      t2[f * N2 + q] = v;
+    });
+    __syncthreads();
+    if (FK != BK_TRANSFORM) {
+      rows_pass<N>(sB, t2, nf, [&](int f, int j, int r, double v) { t1[f * N2 + j * N + r] = v; });
+      __syncthreads();
+      rows_pass<N>(sB, t1, nf, [&](int f, int j, int r, double v) { t2[f * N2 + j * N + r] = v; });
+      __syncthreads();
+    }
+    for (int it = threadIdx.x; it < nf * N2; it += blockDim.x) {
+      const int64_t gi = f0 * N2 + it;
+      const int kind = finfo_kind(sInf[it / N2]);
+      double z = t2[it];
+      if (FK != BK_TRANSFORM && kind == HDGB_DIRICHLET) z = 0.0;  // zero_dirichlet (preconditioner.py:107)
+      a.out[gi] = z;
+      if (FK == BK_INIT) a.p[gi] = z;
+      if ((FK == BK_INIT || FK == BK_UPDATE) && kind_counts(kind)) rz = fma(sIn[it], z, rz);
+    }
+    __syncthreads();
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  if (FK == BK_INIT || FK == BK_UPDATE) {
+    double dummy = 0.0;
+    block_sum2(rz, dummy);
+    if (publish_last(a.part, rz, 0.0, &a.st->cnt[3])) {
+      double trz, t0;
+      final_sum2(a.part, gridDim.x, trz, t0);
+      if (threadIdx.x == 0) {
+        if (FK == BK_INIT) cg_init_z(a.st, trz);
+        else cg_update_z(a.st, trz);
+      }
+    }
+  }
+}
+
+// ================================================================ CG helpers
 // <p, w> from the per-face dots of the operator kernel -> alpha (solver.py:303-310)
 __global__ void __launch_bounds__(HDGB_NT) reduce_pw_kernel(const double* __restrict__ facedot, int64_t nf,
                                                             double* part, CGState* st) {
@@ -314,7 +278,7 @@ __global__ void p_update_kernel(const double* __restrict__ z, double* __restrict
     p[i] = z[i] + beta * p[i];
 }
 
-// ---------------------------------------------------------------- generic vectors
+// ================================================================ generic vectors
 __global__ void __launch_bounds__(HDGB_NT) dot_kernel(const double* __restrict__ x, const double* __restrict__ y,
                                                       int64_t n, double* part, uint32_t* cnt, double* result) {
   double s = 0.0, dummy = 0.0;
@@ -334,7 +298,7 @@ __global__ void axpby_kernel(int64_t n, double a, const double* x, double b, con
     out[i] = a * x[i] + b * y[i];
 }
 
-// ---------------------------------------------------------------- pack / unpack / masks
+// ================================================================ pack / unpack / masks
 // packed position of an unknown face (mesh.py:318-321 ordering), -1 for Dirichlet
 __device__ __forceinline__ int64_t packed_face(const Geo& g, int d, int64_t f) {
   int plane, t1, t2;
@@ -390,7 +354,7 @@ __global__ void halo_kernel(Geo g, int N2, int plane, double* all, double* buf) 
   }
 }
 
-// ---------------------------------------------------------------- table builds
+// ================================================================ table builds
 // Eigenspace self-coupling contribution of element (al, dz) on direction d, side l at
 // tangential eigen-index (b, c) (preconditioner.py:36-55).
 __device__ double y_contrib(const double* tab, int N, const double* dz, bool uniform, double lam, const double* al,
@@ -416,7 +380,7 @@ __device__ double y_contrib(const double* tab, int N, const double* dz, bool uni
   return ad * tab[to.gcc + l] - (ad * ad) * s;
 }
 
-__device__ void elem_alpha(const Geo& g, const double* widths, int i, int j, int k, double* al) {
+__device__ void elem_alpha_w(const Geo& g, const double* widths, int i, int j, int k, double* al) {
   double h1 = widths[i], h2 = widths[g.n1 + j], h3 = widths[g.n1 + g.n2 + k];
   double a0 = h1 * h2 * h3 / 8.0, t1 = 2.0 / h1, t2 = 2.0 / h2, t3 = 2.0 / h3;
   al[0] = a0;
@@ -444,7 +408,7 @@ __global__ void build_y_kernel(Geo g, int N, const double* tab, const double* dz
       int d = fi >= g.foff[2] ? 2 : (fi >= g.foff[1] ? 1 : 0);
       int plane, t1, t2;
       face_coords(g, d, fi - g.foff[d], plane, t1, t2);
-      // element coordinates of the face's low-side (A) and high-side (B) elements
+      // element coordinates of the elements above (B: face is its low face) and below (A)
       int cB[3], cA[3];
       if (d == 0) { cB[0] = plane; cB[1] = t1; cB[2] = t2; }
       else if (d == 1) { cB[0] = t1; cB[1] = plane; cB[2] = t2; }
@@ -452,18 +416,14 @@ __global__ void build_y_kernel(Geo g, int N, const double* tab, const double* dz
       cA[0] = cB[0]; cA[1] = cB[1]; cA[2] = cB[2];
       cA[d] -= 1;
       const int nd = nd_of(g, d);
-      const int kl = g.kind[2 * d], kh = g.kind[2 * d + 1];
-      // slab-interface planes carry both elements' contributions only when both are local;
-      // the multi-GPU layer fills interface faces separately.
-      (void)kl; (void)kh;
       double al[4];
       double acc = 0.0;
-      if (plane < nd) {  // this face is the low face of element B (contributes side 0 first)
-        elem_alpha(g, widths, cB[0], cB[1], cB[2], al);
+      if (plane < nd) {  // low face of element B: side-0 contribution accumulates first
+        elem_alpha_w(g, widths, cB[0], cB[1], cB[2], al);
         acc += y_contrib(tab, N, nullptr, false, lam, al, d, 0, b, c);
       }
       if (plane > 0) {
-        elem_alpha(g, widths, cA[0], cA[1], cA[2], al);
+        elem_alpha_w(g, widths, cA[0], cA[1], cA[2], al);
         acc += y_contrib(tab, N, nullptr, false, lam, al, d, 1, b, c);
       }
       v = acc;
@@ -520,62 +480,7 @@ __global__ void recip_kernel(const double* in, double* out, int64_t n) {
     out[i] = 1.0 / in[i];
 }
 
-// ---------------------------------------------------------------- launchers
-static int grid_for(int64_t work, int per) {
-  int64_t b = (work + per - 1) / per;
-  if (b > 148 * 8) b = 148 * 8;
-  return (int)(b < 1 ? 1 : b);
-}
-
-template <int N, int PREC, int FK>
-static cudaError_t face_launch(hdgb_ctx* c, FaceArgs a, cudaStream_t s, int grid) {
-  using C = FaceCfg<N>;
-  size_t smem = sizeof(double) * C::smem_doubles();
-  auto k = face_kernel<N, PREC, FK>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k<<<grid, HDGB_NT, smem, s>>>(a);
-  c->launches++;
-  return cudaGetLastError();
-}
-
-template <int N, int FK>
-static cudaError_t face_dispatch_prec(hdgb_ctx* c, int prec, FaceArgs a, cudaStream_t s, int grid) {
-  switch (prec) {
-    case HDGB_PREC_NONE: return face_launch<N, HDGB_PREC_NONE, FK>(c, a, s, grid);
-    case HDGB_PREC_BLOCK: return face_launch<N, HDGB_PREC_BLOCK, FK>(c, a, s, grid);
-    case HDGB_PREC_DIAG_NODAL: return face_launch<N, HDGB_PREC_DIAG_NODAL, FK>(c, a, s, grid);
-    case HDGB_PREC_DIAG_EIGEN: return face_launch<N, HDGB_PREC_DIAG_EIGEN, FK>(c, a, s, grid);
-  }
-  return cudaErrorInvalidValue;
-}
-
-template <int N>
-static cudaError_t face_n(hdgb_ctx* c, int fk, int prec, FaceArgs a, cudaStream_t s) {
-  int grid = c->g.ne > 0 ? (int)min((int64_t)HDGB_RED_BLOCKS * 2, (a.nfaces + FaceCfg<N>::FPC - 1) / FaceCfg<N>::FPC) : 1;
-  if (grid < 1) grid = 1;
-  switch (fk) {
-    case FK_PREC: return face_dispatch_prec<N, FK_PREC>(c, prec, a, s, grid);
-    case FK_TRANSFORM: return face_launch<N, HDGB_PREC_NONE, FK_TRANSFORM>(c, a, s, grid);
-    case FK_CG_INIT: return face_dispatch_prec<N, FK_CG_INIT>(c, prec, a, s, grid);
-    case FK_CG_UPDATE: return face_dispatch_prec<N, FK_CG_UPDATE>(c, prec, a, s, grid);
-  }
-  return cudaErrorInvalidValue;
-}
-
-static cudaError_t face_any(hdgb_ctx* c, int fk, int prec, FaceArgs a, cudaStream_t s) {
-  switch (c->N) {
-#define HDGB_CASE(n) \
-  case n:            \
-    return face_n<n>(c, fk, prec, a, s);
-    HDGB_CASE(2) HDGB_CASE(3) HDGB_CASE(4) HDGB_CASE(5) HDGB_CASE(6) HDGB_CASE(7) HDGB_CASE(8) HDGB_CASE(9)
-    HDGB_CASE(10) HDGB_CASE(11) HDGB_CASE(12) HDGB_CASE(13) HDGB_CASE(14) HDGB_CASE(15) HDGB_CASE(16)
-    HDGB_CASE(17)
-#undef HDGB_CASE
-  }
-  return cudaErrorInvalidValue;
-}
-
+// ================================================================ launchers
 static FaceArgs base_args(hdgb_ctx* c, int prec) {
   FaceArgs a = {};
   a.g = c->g;
@@ -597,19 +502,99 @@ static FaceArgs base_args(hdgb_ctx* c, int prec) {
   return a;
 }
 
+template <int N, int PREC, int FK, bool WITHZ>
+static cudaError_t pw_launch(hdgb_ctx* c, const FaceArgs& a, cudaStream_t s) {
+  const int64_t n = c->n_all;
+  int grid = (int)min((int64_t)PW_GRID, (n + 256 * PW_U - 1) / (256 * PW_U));
+  if (grid < 1) grid = 1;
+  pw_kernel<N, PREC, FK, WITHZ><<<grid, 256, 0, s>>>(a, c->d_finfo, (unsigned)n);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+template <int N, int FK, bool WITHZ>
+static cudaError_t pw_prec(hdgb_ctx* c, int prec, const FaceArgs& a, cudaStream_t s) {
+  switch (prec) {
+    case HDGB_PREC_NONE: return pw_launch<N, HDGB_PREC_NONE, FK, WITHZ>(c, a, s);
+    case HDGB_PREC_DIAG_NODAL: return pw_launch<N, HDGB_PREC_DIAG_NODAL, FK, WITHZ>(c, a, s);
+    case HDGB_PREC_DIAG_EIGEN: return pw_launch<N, HDGB_PREC_DIAG_EIGEN, FK, WITHZ>(c, a, s);
+    case HDGB_PREC_BLOCK: return pw_launch<N, HDGB_PREC_NONE, FK, false>(c, a, s);  // r only; block follows
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int N, int FK>
+static cudaError_t blk_launch(hdgb_ctx* c, const FaceArgs& a, cudaStream_t s) {
+  using C = BlkCfg<N>;
+  const size_t smem = sizeof(double) * C::smem_doubles();
+  auto k = blk_kernel<N, FK>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t nb = (c->nfaces + C::FPC - 1) / C::FPC;
+  int grid = (int)min((int64_t)PW_GRID, nb);
+  if (grid < 1) grid = 1;
+  k<<<grid, 256, smem, s>>>(a, c->d_finfo);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+enum { OP_PREC = 0, OP_TRANSFORM = 1, OP_CG_INIT = 2, OP_CG_UPDATE = 3 };
+
+template <int N>
+static cudaError_t face_n(hdgb_ctx* c, int op, int prec, const FaceArgs& a, cudaStream_t s) {
+  cudaError_t e;
+  switch (op) {
+    case OP_TRANSFORM:
+      return blk_launch<N, BK_TRANSFORM>(c, a, s);
+    case OP_PREC:
+      if (prec == HDGB_PREC_BLOCK) return blk_launch<N, BK_PREC>(c, a, s);
+      return pw_prec<N, PW_PREC, true>(c, prec, a, s);
+    case OP_CG_INIT:
+      if ((e = pw_prec<N, PW_INIT, true>(c, prec, a, s)) != cudaSuccess) return e;
+      if (prec == HDGB_PREC_BLOCK) {
+        FaceArgs b = a;
+        b.in = a.r;  // z = P r, p = z, <r,z>
+        return blk_launch<N, BK_INIT>(c, b, s);
+      }
+      return cudaSuccess;
+    case OP_CG_UPDATE:
+      if ((e = pw_prec<N, PW_UPDATE, true>(c, prec, a, s)) != cudaSuccess) return e;
+      if (prec == HDGB_PREC_BLOCK) {
+        FaceArgs b = a;
+        b.in = a.r;
+        return blk_launch<N, BK_UPDATE>(c, b, s);
+      }
+      return cudaSuccess;
+  }
+  return cudaErrorInvalidValue;
+}
+
+static cudaError_t face_any(hdgb_ctx* c, int op, int prec, const FaceArgs& a, cudaStream_t s) {
+  switch (c->N) {
+#define HDGB_CASE(n) \
+  case n:            \
+    return face_n<n>(c, op, prec, a, s);
+    HDGB_CASE(2) HDGB_CASE(3) HDGB_CASE(4) HDGB_CASE(5) HDGB_CASE(6) HDGB_CASE(7) HDGB_CASE(8) HDGB_CASE(9)
+    HDGB_CASE(10) HDGB_CASE(11) HDGB_CASE(12) HDGB_CASE(13) HDGB_CASE(14) HDGB_CASE(15) HDGB_CASE(16)
+    HDGB_CASE(17)
+#undef HDGB_CASE
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_face_transform(hdgb_ctx* c, const double* A_dev, const double* in, double* out, cudaStream_t s) {
   FaceArgs a = base_args(c, HDGB_PREC_NONE);
   a.A = A_dev;
   a.in = in;
   a.out = out;
-  return face_any(c, FK_TRANSFORM, HDGB_PREC_NONE, a, s);
+  return face_any(c, OP_TRANSFORM, HDGB_PREC_NONE, a, s);
 }
 
 cudaError_t launch_prec(hdgb_ctx* c, int kind, const double* in, double* out, cudaStream_t s) {
   FaceArgs a = base_args(c, kind);
   a.in = in;
   a.out = out;
-  return face_any(c, FK_PREC, kind, a, s);
+  return face_any(c, OP_PREC, kind, a, s);
 }
 
 cudaError_t launch_diag_user(hdgb_ctx* c, const double* diag, const double* in, double* out, cudaStream_t s) {
@@ -618,7 +603,7 @@ cudaError_t launch_diag_user(hdgb_ctx* c, const double* diag, const double* in, 
   a.yfull = diag;
   a.in = in;
   a.out = out;
-  return face_any(c, FK_PREC, HDGB_PREC_DIAG_EIGEN, a, s);
+  return face_any(c, OP_PREC, HDGB_PREC_DIAG_EIGEN, a, s);
 }
 
 cudaError_t launch_expand_table(hdgb_ctx* c, int kind, double* out, cudaStream_t s) {
@@ -641,7 +626,7 @@ cudaError_t launch_cg_init(hdgb_ctx* c, int kind, cudaStream_t s) {
   a.r = v + V_R * n;
   a.out = v + V_Z * n;
   a.p = v + V_P * n;
-  return face_any(c, FK_CG_INIT, kind, a, s);
+  return face_any(c, OP_CG_INIT, kind, a, s);
 }
 
 cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s) {
@@ -653,7 +638,7 @@ cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s) {
   a.r = v + V_R * n;
   a.w = v + V_W * n;
   a.out = v + V_Z * n;
-  return face_any(c, FK_CG_UPDATE, kind, a, s);
+  return face_any(c, OP_CG_UPDATE, kind, a, s);
 }
 
 cudaError_t launch_reduce_pw(hdgb_ctx* c, cudaStream_t s) {

@@ -134,6 +134,107 @@ struct FaceArgs {
   CGState* st;
 };
 
+// ---------------------------------------------------------------- deterministic reductions
+// Block sum of two values with a fixed tree; result valid in thread 0.
+__device__ __forceinline__ void block_sum2(double& a, double& b) {
+  __shared__ double ra[32], rb[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  __syncthreads();
+  if (lane == 0) {
+    ra[w] = a;
+    rb[w] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sa = 0.0, sb = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+      sa += ra[q];
+      sb += rb[q];
+    }
+    a = sa;
+    b = sb;
+  }
+}
+
+// Publish this CTA's partials; true in the CTA that arrives last (fixed grid -> fixed order).
+__device__ __forceinline__ bool publish_last(double* part, double a, double b, uint32_t* cnt) {
+  __shared__ bool am_last;
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+    __threadfence();
+    unsigned t = atomicInc(cnt, gridDim.x - 1);
+    am_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (am_last) __threadfence();
+  return am_last;
+}
+
+// Fixed-order sum of all CTA partials (run by the last CTA); valid in thread 0.
+__device__ __forceinline__ void final_sum2(const double* part, int nb, double& a, double& b) {
+  double sa = 0.0, sb = 0.0;
+  for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+    sa += __ldcg(part + 2 * q);
+    sb += __ldcg(part + 2 * q + 1);
+  }
+  block_sum2(sa, sb);
+  a = sa;
+  b = sb;
+}
+
+// PCG scalar recurrences (solver.py:290-321), run by thread 0 of the last CTA.
+__device__ __forceinline__ void cg_init_r(CGState* st, double rr) {  // r0 = F - K x0
+  const double rn = sqrt(rr);
+  st->rr = rr;
+  st->norm0 = rn;
+  st->rn = rn;
+  st->it = 0;
+  if (!isfinite(rn)) {
+    st->status = HDGB_ENONFINITE;
+    st->done = 1;
+  } else if (rn == 0.0 || rn <= st->atol) {
+    st->converged = 1;
+    st->done = 1;
+    st->relres = 0.0;
+  } else {
+    st->thr = fmax(st->rtol * rn, st->atol);
+    st->relres = 1.0;
+  }
+}
+__device__ __forceinline__ void cg_init_z(CGState* st, double rz) { st->rho = rz; st->rz = rz; }
+__device__ __forceinline__ void cg_update_r(CGState* st, double rr) {  // after x += a p, r -= a w
+  const double rn = sqrt(rr);
+  st->rr = rr;
+  st->it += 1;
+  st->rn = rn;
+  if (!isfinite(rn)) {
+    st->status = HDGB_ENONFINITE;
+    st->done = 1;
+  } else if (rn <= st->thr) {
+    st->converged = 1;
+    st->done = 1;
+    st->relres = rn / st->norm0;
+  } else {
+    st->relres = rn / st->norm0;
+    if (st->it >= st->max_iters) st->done = 1;
+  }
+}
+__device__ __forceinline__ void cg_update_z(CGState* st, double rz) {  // beta = rho'/rho
+  st->rz = rz;
+  st->beta = rz / st->rho;
+  st->rho = rz;
+}
+
+// per-face info byte: kind (bits 0-2) | (d*3 + class) << 3
+__host__ __device__ inline int finfo_kind(uint8_t f) { return f & 7; }
+__host__ __device__ inline int finfo_cls(uint8_t f) { return f >> 3; }
+
 }  // namespace hdgb
 
 struct hdgb_ctx {
@@ -156,6 +257,7 @@ struct hdgb_ctx {
   double* d_dn_full = nullptr;
   double* d_xbuf = nullptr;
   uint32_t* d_tickets = nullptr;
+  uint8_t* d_finfo = nullptr;     // per-face kind/class byte
   double* d_facedot = nullptr;
   double* d_part = nullptr;
   double* d_A = nullptr;          // transform matrix scratch N*N
@@ -169,6 +271,7 @@ struct hdgb_ctx {
   int graph_iters = 0;
   int64_t launches = 0;
   int smem_op = 0;
+  int64_t slab_bytes = 48LL << 20;  // L2 working-set target of one z-slab of the colour passes
 };
 
 namespace hdgb {
@@ -180,6 +283,9 @@ cudaError_t launch_op(hdgb_ctx* c, int variant, int mode, const double* u, doubl
 cudaError_t launch_face_transform(hdgb_ctx* c, const double* A_dev, const double* in, double* out, cudaStream_t s);
 cudaError_t launch_prec(hdgb_ctx* c, int kind, const double* in, double* out, cudaStream_t s);
 cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s);
+cudaError_t launch_cg_init(hdgb_ctx* c, int kind, cudaStream_t s);
+cudaError_t launch_diag_user(hdgb_ctx* c, const double* diag, const double* in, double* out, cudaStream_t s);
+int grid_for(int64_t work, int per);
 cudaError_t launch_build_tables(hdgb_ctx* c, cudaStream_t s);
 cudaError_t op_set_smem_limits(hdgb_ctx* c);
 }  // namespace hdgb
