@@ -271,7 +271,10 @@ struct hdgb_ctx {
   int graph_iters = 0;
   int64_t launches = 0;
   int smem_op = 0;
-  int64_t slab_bytes = 48LL << 20;  // L2 working-set target of one z-slab of the colour passes
+  // L2 working-set target of one z-slab of the colour passes; 0 = one slab.  Slabbing cuts
+  // HBM traffic (pass-0 partials stay in L2) but multiplies launches; while the element
+  // kernels are issue-bound the single slab is faster (HDGB_SLAB_MB overrides).
+  int64_t slab_bytes = 0;
 };
 
 namespace hdgb {
