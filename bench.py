@@ -193,6 +193,45 @@ def _timed_apply(dc, u, r, variant, steps, warmup, flush, stream):
     return ms, dc.launches() - l0
 
 
+def _large_point(hb, p, m, lam, flush, stream, hbm, fp64_peak, reps=10):
+    """Apply timings (plain, transformed, block and eigen-diagonal preconditioners) on an m^3 grid."""
+    import torch
+
+    mesh = hb.Mesh((m, m, m))
+    ctx = hb.make_context(mesh, p, hb.SolverConfig(lam=lam))
+    dc = hb.device_context(ctx)
+    n = p + 1
+    N, N_all = mesh.n_trace_unknowns(p), mesh.n_all(p)
+    u = dc.unpack(torch.from_numpy(np.random.default_rng(p).uniform(-1.0, 1.0, N)).cuda())
+    r = dc.empty()
+    out = {"p": p, "elements": mesh.n_elements, "trace_unknowns": N}
+    ops = {"plain": lambda: dc.apply(u, 0, out=r), "transformed": lambda: dc.apply(u, 1, out=r),
+           "block_prec": lambda: dc.prec(u, 1, out=r), "eigen_diag_prec": lambda: dc.prec(u, 3, out=r)}
+    for name, fn in ops.items():
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b) * 1e-3)
+        t = statistics.median(ts)
+        ent = {"us": t * 1e6, "trace_dof_per_s": N / t, "hbm_frac": 16 * N_all / t / 1e9 / hbm}
+        if name == "plain":
+            ent["fp64_frac"] = mesh.n_elements * (73 * n ** 3 + 12 * n ** 2) / t / 1e12 / fp64_peak
+        if name == "transformed":
+            ent["fp64_frac"] = mesh.n_elements * (25 * n ** 3 + 12 * n ** 2) / t / 1e12 / fp64_peak
+        out[name] = ent
+    del dc, ctx, u, r
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -340,6 +379,31 @@ def run_ours(args):
               "note": "whole solve incl. setup kernels, one CUDA graph with device-side while loop; "
                       "config-2 vectors are L2-resident during the solve"}
 
+    # ---- FP64 view of the plain operator (FP64-bound for p >~ 3; reference FlopCounter counts)
+    import ctypes
+
+    from paper_2007_11891_b200 import _lib
+
+    fp64_peak = ctypes.c_double()
+    _lib.check(_lib.lib().hdgb_fp64_peak(ctypes.byref(fp64_peak), ctypes.c_void_p(stream.cuda_stream)))
+    fl_plain = mesh.n_elements * (73 * n ** 3 + 12 * n ** 2)
+    fl_trans = mesh.n_elements * (25 * n ** 3 + 12 * n ** 2)
+    fp64 = {"peak_tflops_measured": fp64_peak.value,
+            "plain_tflops": fl_plain / t_k / 1e12, "plain_frac": fl_plain / t_k / 1e12 / fp64_peak.value,
+            "transformed_tflops": fl_trans / t_tr / 1e12,
+            "transformed_frac": fl_trans / t_tr / 1e12 / fp64_peak.value,
+            "flops": "reference FlopCounter: n_e(73n^3+12n^2) plain, n_e(25n^3+12n^2) transformed"}
+
+    # ---- large single-GPU workloads (BASELINE configs[2] p-sweep, ~2e7 unknowns; config 5)
+    large = {}
+    if world == 1 and not args.no_large:
+        sizes = {2: 91, 3: 75, 4: 65, 6: 52, 8: 44, 12: 34, 16: 29}
+        ps = [2, 3, 4, 6, 8, 12, 16] if args.sweep else [8]
+        for p3 in ps:
+            large[f"config3_p{p3}"] = _large_point(hb, p3, sizes[p3], 0.0, flush, stream, hbm, fp64_peak.value)
+        if args.config5:
+            large["config5_128^3_p8"] = _large_point(hb, 8, 128, 1.0, flush, stream, hbm, fp64_peak.value, reps=5)
+
     # ---- CPU oracle on this host (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -361,11 +425,15 @@ def run_ours(args):
                    "l2": "flushed before every timed step (512 MB write)", "parallelism": f"x-slab dp{world}"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": (traffic or {}).get("bytes_per_launch"),
-                     "kernel": "op_kernel<9,plain,apply>", "kernel_ms": t_k * 1e3,
-                     "algorithmic_bytes_per_launch": alg_bytes, "peak_kind": peak_kind},
+                     "kernel": "op_kernel<9,plain> colour pass 0 + pass 1 (one apply = 2 launches)",
+                     "kernel_ms": t_k * 1e3,
+                     "algorithmic_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
+                     "note": "'launch' = one apply (both colour passes); 16 B per all-face DOF"},
+        "fp64": fp64,
         "transformed_apply": {"value": N / t_tr, "unit": "trace-DOF/s", "kernel_ms": t_tr * 1e3,
                               "hbm_frac": (alg_bytes / t_tr / 1e9) / hbm},
         "cg": cg,
+        "large": large,
         "cpu_baseline": cpu,
         "e2e": {"value": world * N / t_e2e, "unit": "trace-DOF/s", "h2d_bytes_per_step": 8 * N_all,
                 "d2h_bytes_per_step": 8 * N_all, "ms_per_step": t_e2e * 1e3,
@@ -388,6 +456,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-large", action="store_true", help="skip the config-3 (p=8, 44^3) measurement")
+    ap.add_argument("--sweep", action="store_true", help="full config-3 degree sweep p=2..16")
+    ap.add_argument("--config5", action="store_true", help="also time config 5 (128^3, p=8, 4 GB vectors)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -130,6 +130,10 @@ int hdgb_halo_add(hdgb_ctx* ctx, double* all, int plane, const double* buf, void
 /* Number of kernels launched by this ctx so far (evidence counter for bench.py). */
 int64_t hdgb_ctx_launches(const hdgb_ctx* ctx);
 
+/* Diagnostics: measured dense DFMA throughput of the current device in TFLOP/s (FP64 roofline
+ * denominator for the compute-bound plain operator; MEASURED_PEAKS.json has no FP64 entry). */
+int hdgb_fp64_peak(double* tflops, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,6 +18,7 @@ cudaError_t launch_pack(hdgb_ctx* c, int mode, const double* in, double* out, cu
 cudaError_t launch_halo(hdgb_ctx* c, int mode, int plane, double* all, double* buf, cudaStream_t s);
 cudaError_t launch_diag_user(hdgb_ctx* c, const double* diag, const double* in, double* out, cudaStream_t s);
 cudaError_t launch_expand_table(hdgb_ctx* c, int kind, double* out, cudaStream_t s);
+cudaError_t measure_fp64_peak(double* tflops, cudaStream_t s);
 
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
@@ -299,6 +300,12 @@ int hdgb_debug_op_cg(hdgb_ctx* c, int variant, const double* u, double* r, doubl
   HDGB_CUDA(cudaMemsetAsync(c->d_st, 0, sizeof(CGState), s));
   HDGB_CUDA(launch_op(c, variant, MODE_CG, u, r, s));
   HDGB_CUDA(cudaMemcpyAsync(facedot_out, c->d_facedot, sizeof(double) * c->nfaces, cudaMemcpyDeviceToDevice, s));
+  return HDGB_OK;
+}
+
+int hdgb_fp64_peak(double* tflops, void* stream) {
+  if (!tflops) return einval("null argument");
+  HDGB_CUDA(measure_fp64_peak(tflops, (cudaStream_t)stream));
   return HDGB_OK;
 }
 

@@ -480,6 +480,47 @@ __global__ void recip_kernel(const double* in, double* out, int64_t n) {
     out[i] = 1.0 / in[i];
 }
 
+// ================================================================ diagnostics
+// 8 independent DFMA chains per thread: issue-bound on the FP64 pipe.
+__global__ void __launch_bounds__(256) dfma_peak_kernel(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) out[blockIdx.x] = s;  // keep the chains alive
+}
+
+cudaError_t measure_fp64_peak(double* tflops, cudaStream_t s) {
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = sms * 8, iters = 4096;
+  double* out = nullptr;
+  cudaError_t e = cudaMalloc(&out, sizeof(double) * blocks);
+  if (e != cudaSuccess) return e;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  dfma_peak_kernel<<<blocks, 256, 0, s>>>(out, iters, 0.999999, 1e-7);  // warm-up
+  cudaEventRecord(a, s);
+  dfma_peak_kernel<<<blocks, 256, 0, s>>>(out, iters, 0.999999, 1e-7);
+  cudaEventRecord(b, s);
+  e = cudaEventSynchronize(b);
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  *tflops = 2.0 * 8.0 * iters * (double)blocks * 256 / (ms * 1e-3) / 1e12;
+  return e;
+}
+
 // ================================================================ launchers
 static FaceArgs base_args(hdgb_ctx* c, int prec) {
   FaceArgs a = {};
