@@ -467,10 +467,17 @@ struct OpTCfg {
   static constexpr bool DZ_SMEM = N <= 13;
   static constexpr bool BS_REG = N <= 12;
   static constexpr int TAB = (2 * N + 2 + 1) / 2 * 2 + (DZ_SMEM ? (N * N2 + 1) / 2 * 2 : 0);
-  __host__ __device__ static constexpr int per_elem(int color) { return 6 * N2 * (color ? 2 : 1) + US; }
+#ifndef HDGB_OPT_WMAX
+#define HDGB_OPT_WMAX 8  // warps per CTA (256 threads -> up to 255 registers per thread)
+#endif
+#ifndef HDGB_OPT_DB
+#define HDGB_OPT_DB 0  // measured: occupancy beats prefetch depth here (p=8: 321 vs 359 us)
+#endif
+  static constexpr bool DB = HDGB_OPT_DB;  // double-buffered face staging (prefetch next group)
+  __host__ __device__ static constexpr int per_elem(int) { return 6 * N2 * (DB ? 2 : 1) + US; }
   __host__ __device__ static constexpr int W(int color) {
     // 198 KB dynamic: leaves room for the static per-face dot scratch (<= 24 KB)
-    return cmax(1, cmin(16, (198 * 1024 / 8 - TAB) / (EPW * per_elem(color))));
+    return cmax(1, cmin(HDGB_OPT_WMAX, (198 * 1024 / 8 - TAB) / (EPW * per_elem(color))));
   }
   __host__ __device__ static constexpr int smem_doubles(int color) { return TAB + W(color) * EPW * per_elem(color); }
 };
@@ -499,9 +506,8 @@ __global__ void __launch_bounds__(OpTCfg<N>::W(COLOR) * 32) opT_kernel(OpArgs a,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int el = lane / N, m = lane - (lane / N) * N;
   const bool lane_on = el < EPW;
-  double* sIn = smem + C::TAB + (warp * EPW + (lane_on ? el : 0)) * PE;  // [d][q][side]
-  double* sR = sIn + 6 * N2;                                              // [s][q] (pass 1)
-  double* sU = sIn + 6 * N2 * (COLOR ? 2 : 1);                            // 2 U planes [a2][a3]
+  double* sIn0 = smem + C::TAB + (warp * EPW + (lane_on ? el : 0)) * PE;  // [d][q][side] (x2 if DB)
+  double* sU = sIn0 + (C::DB ? 2 : 1) * 6 * N2;                          // 2 U planes [a2][a3]
 
   double bs0[C::BS_REG ? N : 1], bs1[C::BS_REG ? N : 1];
   if (C::BS_REG) {
@@ -516,45 +522,61 @@ __global__ void __launch_bounds__(OpTCfg<N>::W(COLOR) * 32) opT_kernel(OpArgs a,
   const double gcc0 = sGcc[0], gcc1 = sGcc[1];
 
   const int64_t nw = (int64_t)gridDim.x * W;
-  for (int64_t T = (int64_t)blockIdx.x * W + warp; t0 + T * EPW < t1; T += nw) {
-    const int64_t t = t0 + T * EPW + el;
-    Elem E;
-    const bool have = lane_on && t < t1 && pair_elem(g, t, COLOR, E);
-    if (have) {
+  // gather of one element's faces into an (interleaved) staging buffer
+  auto issue = [&](const Elem& Ei, double* buf) {
 #pragma unroll
-      for (int s = 0; s < 6; ++s) {
-        const double* src = a.u + E.fid[s] * N2;
-        double* dst = sIn + (s >> 1) * N2 * 2 + (s & 1);
-        for (int q = m; q < N2; q += N) cp_async8(dst + 2 * q, src + q);
-        if (COLOR == 1 && (E.shared >> s & 1u)) {
-          const double* rs = a.r + E.fid[s] * N2;
-          for (int q = m; q < N2; q += N) cp_async8(sR + s * N2 + q, rs + q);
-        }
-      }
+    for (int s = 0; s < 6; ++s) {
+      const double* src = a.u + Ei.fid[s] * N2;
+      double* dst = buf + (s >> 1) * N2 * 2 + (s & 1);
+      for (int q = m; q < N2; q += N) cp_async8(dst + 2 * q, src + q);
     }
+  };
+  int64_t T = (int64_t)blockIdx.x * W + warp;
+  Elem E, En;
+  bool have = lane_on && t0 + T * EPW + el < t1 && pair_elem(g, t0 + T * EPW + el, COLOR, E);
+  if (have) issue(E, sIn0);
+  cp_async_commit();
+  for (int buf = 0; t0 + T * EPW < t1; T += nw, buf ^= 1) {
+    double* sIn = sIn0 + buf * (C::DB ? 6 * N2 : 0);
+    // prefetch the next element group of this warp into the other buffer
+    const int64_t tn = t0 + (T + nw) * EPW + el;
+    const bool have_n = lane_on && t0 + (T + nw) * EPW < t1 && tn < t1 && pair_elem(g, tn, COLOR, En);
+    if (C::DB && have_n) issue(En, sIn0 + (buf ^ 1) * 6 * N2);
     cp_async_commit();
-    cp_async_wait_all();
-    __syncwarp();
     double al[4] = {0.0, 0.0, 0.0, 0.0};
     int kinds[6];
+    double* fb[6];
+    double cf[6];
+    bool sh[6];
     double dots[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    // contribution c = alpha_d GCC_ll u - g (+ colour-0 partial) stored to r (operator.py:243-257)
-    auto emit = [&](int s, int q, double gval, double uval) {
-      const int d = s >> 1, side = s & 1;
-      const bool sh = E.shared >> s & 1u;
-      double val = (al[1 + d] * (side ? gcc1 : gcc0)) * uval - gval;
-      if (COLOR == 1 && sh) val = sR[s * N2 + q] + val;
-      if ((MODE & 1) && (COLOR == 1 || !sh)) {
-        if (kinds[s] == HDGB_DIRICHLET) val = 0.0;
-        if (kind_counts(kinds[s])) dots[s] = fma(uval, val, dots[s]);
-      }
-      a.r[E.fid[s] * N2 + q] = val;
-    };
     if (have) {
       elem_alpha(a, E.c, al);
 #pragma unroll
-      for (int s = 0; s < 6; ++s) kinds[s] = face_kind(g, s >> 1, E.c[s >> 1] + (s & 1));
+      for (int s = 0; s < 6; ++s) {
+        kinds[s] = face_kind(g, s >> 1, E.c[s >> 1] + (s & 1));
+        fb[s] = a.r + E.fid[s] * N2;
+        cf[s] = al[1 + (s >> 1)] * ((s & 1) ? gcc1 : gcc0);
+        sh[s] = E.shared >> s & 1u;
+      }
     }
+    if (C::DB) {
+      asm volatile("cp.async.wait_group 1;\n" ::);  // this group's faces (the next group may be in flight)
+    } else {
+      cp_async_wait_all();
+    }
+    __syncwarp();
+    // contribution c = alpha_d GCC_ll u - g (+ colour-0 partial `prev`) stored to r (operator.py:243-257)
+    auto emit = [&](int s, int q, double gval, double uval, double prev) {
+      double val = cf[s] * uval - gval;
+      if (COLOR == 1 && sh[s]) val = prev + val;
+      if ((MODE & 1) && (COLOR == 1 || !sh[s])) {
+        if (kinds[s] == HDGB_DIRICHLET) val = 0.0;
+        if (kind_counts(kinds[s])) dots[s] = fma(uval, val, dots[s]);
+      }
+      fb[s][q] = val;
+    };
+    // colour-0 partial of face s at q (pass 1, shared faces), read through L2
+    auto prev_of = [&](int s, int q) -> double { return (COLOR == 1 && sh[s]) ? __ldcg(fb[s] + q) : 0.0; };
     {
       const int a3 = m;
       double2 xv[N];
@@ -575,29 +597,43 @@ __global__ void __launch_bounds__(OpTCfg<N>::W(COLOR) * 32) opT_kernel(OpArgs a,
         const double A10 = al[1] * b10, A11 = al[1] * b11;
         const double lam13 = UNI ? 0.0 : lam3 + al[1] * tab[to.Lam + a1];
         double ay0 = 0.0, ay1 = 0.0;
+        double py0 = 0.0, py1 = 0.0, pz0 = 0.0, pz1 = 0.0;
         if (have) {
+          // issue this step's partial loads early; they land while the step computes
+          py0 = prev_of(2, a1 * N + a3);
+          py1 = prev_of(3, a1 * N + a3);
+          pz0 = prev_of(4, a1 * N + m);
+          pz1 = prev_of(5, a1 * N + m);
+          // issue every shared-memory load of the step first (z pairs, dz line), then compute:
+          // keeps the 9 independent a2 chains in flight instead of serialising on one register set
+          double2 zvs[N];
+          double dzs[N];
 #pragma unroll
           for (int a2 = 0; a2 < N; ++a2) {
-            const double2 zv = *reinterpret_cast<const double2*>(sIn + (2 * N2 + a1 * N + a2) * 2);  // z [a1][a2]
+            zvs[a2] = *reinterpret_cast<const double2*>(sIn + (2 * N2 + a1 * N + a2) * 2);  // z [a1][a2]
+            if (UNI) {
+              dzs[a2] = C::DZ_SMEM ? sDz[(a1 * N + a2) * N + a3] : __ldg(a.dz + (a1 * N + a2) * N + a3);
+            } else {
+              dzs[a2] = 1.0 / (lam13 + al[2] * tab[to.Lam + a2]);  // EigenScale3D per element
+            }
+          }
+          const double y0 = al[2] * yv.x, y1 = al[2] * yv.y;
+#pragma unroll
+          for (int a2 = 0; a2 < N; ++a2) {
+            const double2 zv = zvs[a2];
             double F = bz1 * zv.y;
             F = fma(bz0, zv.x, F);
-            F = fma(al[2], fma(BS0(a2), yv.x, BS1(a2) * yv.y), F);
+            F = fma(BS0(a2), y0, fma(BS1(a2), y1, F));
             F = fma(A10, xv[a2].x, fma(A11, xv[a2].y, F));
-            double dz;
-            if (UNI) {
-              dz = C::DZ_SMEM ? sDz[(a1 * N + a2) * N + a3] : __ldg(a.dz + (a1 * N + a2) * N + a3);
-            } else {
-              dz = 1.0 / (lam13 + al[2] * tab[to.Lam + a2]);  // EigenScale3D per element
-            }
-            const double U = F * dz;
+            const double U = F * dzs[a2];
             pl[a2 * N + a3] = U;
             ax0[a2] = fma(b10, U, ax0[a2]);
             ax1[a2] = fma(b11, U, ax1[a2]);
             ay0 = fma(BS0(a2), U, ay0);
             ay1 = fma(BS1(a2), U, ay1);
           }
-          emit(2, a1 * N + a3, al[2] * ay0, yv.x);
-          emit(3, a1 * N + a3, al[2] * ay1, yv.y);
+          emit(2, a1 * N + a3, al[2] * ay0, yv.x, py0);
+          emit(3, a1 * N + a3, al[2] * ay1, yv.y, py1);
         }
         __syncwarp();
         if (have) {
@@ -611,15 +647,21 @@ __global__ void __launch_bounds__(OpTCfg<N>::W(COLOR) * 32) opT_kernel(OpArgs a,
             az1 = fma(BS1(k), v, az1);
           }
           const double2 zv = *reinterpret_cast<const double2*>(sIn + (2 * N2 + a1 * N + m) * 2);
-          emit(4, a1 * N + m, al[3] * az0, zv.x);
-          emit(5, a1 * N + m, al[3] * az1, zv.y);
+          emit(4, a1 * N + m, al[3] * az0, zv.x, pz0);
+          emit(5, a1 * N + m, al[3] * az1, zv.y, pz1);
         }
       }
       if (have) {
+        double px0[N], px1[N];
 #pragma unroll
         for (int a2 = 0; a2 < N; ++a2) {
-          emit(0, a2 * N + a3, al[1] * ax0[a2], xv[a2].x);
-          emit(1, a2 * N + a3, al[1] * ax1[a2], xv[a2].y);
+          px0[a2] = prev_of(0, a2 * N + a3);
+          px1[a2] = prev_of(1, a2 * N + a3);
+        }
+#pragma unroll
+        for (int a2 = 0; a2 < N; ++a2) {
+          emit(0, a2 * N + a3, al[1] * ax0[a2], xv[a2].x, px0[a2]);
+          emit(1, a2 * N + a3, al[1] * ax1[a2], xv[a2].y, px1[a2]);
         }
       }
     }
@@ -632,7 +674,7 @@ __global__ void __launch_bounds__(OpTCfg<N>::W(COLOR) * 32) opT_kernel(OpArgs a,
       if (have && m == 0) {
 #pragma unroll
         for (int s = 0; s < 6; ++s) {
-          if (COLOR == 1 || !(E.shared >> s & 1u)) {
+          if (COLOR == 1 || !sh[s]) {
             double tot = 0.0;
             for (int k = 0; k < N; ++k) tot += sDot[warp][el][s][k];
             a.facedot[E.fid[s]] = tot;
@@ -641,7 +683,12 @@ __global__ void __launch_bounds__(OpTCfg<N>::W(COLOR) * 32) opT_kernel(OpArgs a,
       }
     }
     __syncwarp();  // staging buffers are reused by the next elements
+    if (!C::DB && have_n) issue(En, sIn0);  // single buffer: gather once it is free
+    if (!C::DB) cp_async_commit();
+    E = En;
+    have = have_n;
   }
+  cp_async_wait_all();
 }
 
 template <int N, int MODE, int COLOR>
