@@ -52,10 +52,9 @@ static void free_ctx(hdgb_ctx* c) {
     for (auto& gx : row)
       if (gx) cudaGraphExecDestroy(gx);
   double* bufs[] = {c->d_tab, c->d_dz, c->d_widths, c->d_yinv_cls, c->d_y_cls, c->d_dn_cls, c->d_yinv_full,
-                    c->d_y_full, c->d_dn_full, c->d_xbuf, c->d_facedot, c->d_part, c->d_A, c->d_vec, c->d_io};
+                    c->d_y_full, c->d_dn_full, c->d_hat, c->d_facedot, c->d_part, c->d_fcoef, c->d_vec, c->d_io};
   for (double* b : bufs)
     if (b) cudaFree(b);
-  if (c->d_tickets) cudaFree(c->d_tickets);
   if (c->d_finfo) cudaFree(c->d_finfo);
   if (c->d_st) cudaFree(c->d_st);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -155,6 +154,7 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
   }
   tab[to.gcc] = d->GCC_diag[0];
   tab[to.gcc + 1] = d->GCC_diag[1];
+  c->h_tab = tab;
 
   int rc = HDGB_OK;
 #define CK(call)                          \
@@ -184,26 +184,47 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
     CK(cudaMalloc(&c->d_yinv_full, sizeof(double) * c->n_all));
     CK(cudaMalloc(&c->d_dn_full, sizeof(double) * c->n_all));
   }
-  // scratch for the two-party face assembly: xbuf face stride padded to 128 B
-  c->xstride = ((int64_t)N2 + 15) / 16 * 16;
-  CK(cudaMalloc(&c->d_xbuf, sizeof(double) * c->xstride * c->nfaces));
-  CK(cudaMalloc(&c->d_tickets, sizeof(uint32_t) * c->nfaces));
-  CK(cudaMemset(c->d_tickets, 0, sizeof(uint32_t) * c->nfaces));
+  // plain operator scratch: the eigen-space input (T (x) T) u of the transformed core
+  CK(cudaMalloc(&c->d_hat, sizeof(double) * (c->n_all > 0 ? c->n_all : 1)));
   {
     // one byte per face: kind | (d*3 + class) << 3 (mesh.py:129-137 classification)
+    // and the plain operator's face self-term coefficient: the sum over the element sides
+    // present in this partition of alpha_d GCC_ll (operator.py:243-257)
     std::vector<uint8_t> finfo(c->nfaces);
+    std::vector<double> fcoef(c->nfaces);
+    const int off[3] = {0, g.n1, g.n1 + g.n2};
     for (int q = 0; q < 3; ++q)
       for (int64_t f = 0; f < g.nf[q]; ++f) {
         int plane, t1, t2;
         face_coords(g, q, f, plane, t1, t2);
         finfo[g.foff[q] + f] = (uint8_t)(face_kind(g, q, plane) | ((q * 3 + face_class(g, q, plane)) << 3));
+        int cB[3];
+        if (q == 0) { cB[0] = plane; cB[1] = t1; cB[2] = t2; }
+        else if (q == 1) { cB[0] = t1; cB[1] = plane; cB[2] = t2; }
+        else { cB[0] = t1; cB[1] = t2; cB[2] = plane; }
+        auto alpha = [&](const int* e) {  // ElementGeometry alpha_d (mesh.py:46-56)
+          if (c->uniform) return c->al_u[1 + q];
+          const double h1 = wid[off[0] + e[0]], h2 = wid[off[1] + e[1]], h3 = wid[off[2] + e[2]];
+          const double a0 = h1 * h2 * h3 / 8.0, tt = 2.0 / (q == 0 ? h1 : (q == 1 ? h2 : h3));
+          return a0 * (tt * tt);
+        };
+        const int nd = q == 0 ? g.n1 : (q == 1 ? g.n2 : g.n3);
+        double coef = 0.0;
+        if (plane > 0) {  // element below: its high side (GCC_11)
+          int cA[3] = {cB[0], cB[1], cB[2]};
+          cA[q] -= 1;
+          coef += alpha(cA) * tab[to.gcc + 1];
+        }
+        if (plane < nd) coef += alpha(cB) * tab[to.gcc];  // element above: its low side (GCC_00)
+        fcoef[g.foff[q] + f] = coef;
       }
     CK(cudaMalloc(&c->d_finfo, c->nfaces));
     CK(cudaMemcpy(c->d_finfo, finfo.data(), c->nfaces, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&c->d_fcoef, sizeof(double) * (c->nfaces > 0 ? c->nfaces : 1)));
+    CK(cudaMemcpy(c->d_fcoef, fcoef.data(), sizeof(double) * c->nfaces, cudaMemcpyHostToDevice));
   }
   CK(cudaMalloc(&c->d_facedot, sizeof(double) * c->nfaces));
   CK(cudaMalloc(&c->d_part, sizeof(double) * 4 * HDGB_RED_BLOCKS + 64));
-  CK(cudaMalloc(&c->d_A, sizeof(double) * N2));
   CK(cudaMalloc(&c->d_st, sizeof(CGState)));
   CK(cudaMemset(c->d_st, 0, sizeof(CGState)));
   CK(cudaMallocHost(&c->h_st, sizeof(CGState)));
@@ -282,8 +303,7 @@ int hdgb_face_transform(hdgb_ctx* c, const double* A_host, const double* in, dou
   if (in == out) return einval("input and output must not alias");
   cudaStream_t s = (cudaStream_t)stream;
   // stage A through the ctx (pageable copy is synchronous w.r.t. the host)
-  HDGB_CUDA(cudaMemcpyAsync(c->d_A, A_host, sizeof(double) * c->N * c->N, cudaMemcpyHostToDevice, s));
-  HDGB_CUDA(launch_face_transform(c, c->d_A, in, out, s));
+  HDGB_CUDA(launch_face_transform(c, A_host, in, out, s));
   return HDGB_OK;
 }
 

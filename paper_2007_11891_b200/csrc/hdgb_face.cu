@@ -116,127 +116,260 @@ __global__ void __launch_bounds__(256) pw_kernel(FaceArgs a, const uint8_t* __re
   }
 }
 
-// ================================================================ block / transform kernels
-enum { BK_PREC = 0, BK_INIT = 1, BK_UPDATE = 2, BK_TRANSFORM = 3 };
-
-template <int N>
-struct BlkCfg {
-  static constexpr int N2 = N * N;
-  static constexpr int FPC = (256 / N) > 0 ? (256 / N) : 1;  // faces per batch: rows per pass <= 256
-  static constexpr int V = FPC * N2;
-  static constexpr int TP = N + (N & 1);
-  static constexpr int smem_doubles() { return 2 * N * TP + 4 * V; }
-};
-
-// rows pass over nf faces of X: Y_f[j][r] = sum_b A[j][b] X_f[r][b], stored transposed via store
-template <int N, typename Store>
-__device__ __forceinline__ void rows_pass(const double* __restrict__ A, const double* __restrict__ X, int nf,
-                                          Store store) {
-  constexpr int N2 = N * N, TP = BlkCfg<N>::TP;
-  for (int it = threadIdx.x; it < nf * N; it += blockDim.x) {
-    const int f = it / N, r = it - f * N;
-    double x[N + 1];
-    const double* xr = X + f * N2 + r * N;
-#pragma unroll
-    for (int b = 0; b < N; ++b) x[b] = xr[b];
-    x[N] = 0.0;
-#pragma unroll 1
-    for (int j = 0; j < N; ++j) {
-      const double* Aj = A + j * TP;
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int b = 0; b < N; b += 2) {
-        const double2 t = *reinterpret_cast<const double2*>(Aj + b);
-        s0 = fma(t.x, x[b], s0);
-        s1 = fma(t.y, x[b + 1], s1);
-      }
-      store(f, j, r, s0 + s1);
-    }
-  }
-}
+// ================================================================ face-block kernels
+// Every face block is an N x N tile X (rows = first tangential index).  The kernels apply
+// tensor-product operators (A (x) A) X = A X A^T and the block preconditioner
+// (S (x) S) y^-1 (S^T (x) S^T) (preconditioner.py:96-110) as 1D line passes:
+//  * batches of FPB faces are contiguous in HBM: one elected thread streams them into a
+//    ring of shared-memory stages with bulk async copies (cp.async.bulk + mbarrier
+//    transaction counts), S-1 batches ahead, so the loads cost no issue slots and keep
+//    tens of KB per SM in flight;
+//  * one thread per (face, line): a pass along the first index works on a COLUMN held in
+//    registers, a pass along the second index on a ROW; the four passes of Alg. 4 need only
+//    two exchanges (column -> row -> row -> column) through a padded shared tile whose
+//    faces lie N (mod 16) doubles apart and rows 17 apart, so the column and the row
+//    accesses of a half-warp hit 16 distinct 8-byte bank pairs;
+//  * the 1D matrices are kernel parameters (constant bank): every multiply-add is one DFMA
+//    and each line pass is N independent FMA chains;
+//  * results leave through coalesced stores.
+enum { FX_TRANSFORM = 0, FX_POST = 1, FX_PREC = 2, FX_INIT = 3, FX_UPDATE = 4 };
 
 template <int N, int FK>
-__global__ void __launch_bounds__(256) blk_kernel(FaceArgs a, const uint8_t* __restrict__ finfo) {
-  using C = BlkCfg<N>;
-  constexpr int N2 = C::N2, FPC = C::FPC, V = C::V, TP = C::TP;
-  if ((FK == BK_INIT || FK == BK_UPDATE) && a.st->done) return;
-  extern __shared__ __align__(16) double smem[];
-  double* sA = smem;            // forward matrix [j][b] (S^T, or A)
-  double* sB = sA + N * TP;     // backward matrix (S)
-  double* sIn0 = sB + N * TP;   // 2 x V staged inputs
-  double* t1 = sIn0 + 2 * V;
-  double* t2 = t1 + V;
-  __shared__ uint8_t sInf[FPC];
+struct FxCfg {
+  static constexpr int N2 = N * N;
+  static constexpr int FPB = (256 / N) & ~1;  // faces per batch (even: 16-byte batch offsets)
+  static constexpr int NT = 256;              // threads: one per (face, line), FPB * N <= 256 active
+  static constexpr int NP = 17;               // exchange row pitch, = 1 (mod 16)
+  static constexpr int pad16(int x, int r) { return x + (((r - x) % 16) + 16) % 16; }
+  static constexpr int WP = pad16(N * NP, N % 16);  // exchange face pitch, = N (mod 16)
+  static constexpr int BAT = FPB * N2;              // doubles per staged batch
+  static constexpr int OPS = FK == FX_POST ? 2 : 1; // staged operands (G and u for the epilogue)
+  static constexpr int S = (FK == FX_POST || N >= 12) ? 2 : 3;  // ring stages
+  static constexpr int smem_doubles() { return S * OPS * BAT + FPB * WP; }
+  // register budget: CTAs per SM the shared memory allows anyway
+  static constexpr int MINB = (227 * 1024) / (8 * smem_doubles()) >= 4 ? 4 : ((227 * 1024) / (8 * smem_doubles()) >= 3 ? 3 : 2);
+};
 
-  TabOff to;
-  to.set(N);
-  for (int t = threadIdx.x; t < N * TP; t += blockDim.x) {
-    const int r = t / TP, c = t - r * TP;
-    if (FK == BK_TRANSFORM) {
-      sA[t] = c < N ? a.A[r * N + c] : 0.0;
-    } else {
-      sA[t] = c < N ? a.tab[to.St + r * N + c] : 0.0;  // S^T[r][c]
-      sB[t] = c < N ? a.tab[to.S + r * N + c] : 0.0;   // S[r][c]
+// y[j] = sum_i M[j][i] x[i]: N independent chains, M from the constant bank
+template <int N>
+__device__ __forceinline__ void line_mv(const double* __restrict__ M, const double* x, double* y) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) y[j] = M[j * N] * x[0];
+#pragma unroll
+  for (int i = 1; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) y[j] = fma(M[j * N + i], x[i], y[j]);
+}
+
+// A: forward 1D matrix (S^T, T, MS or the user's A), B: backward (S); FX_POST keeps the
+// quadrature weights in B[0..N-1].
+template <int N>
+struct FxMats {
+  double A[N * N];
+  double B[N * N];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// bulk global -> shared copy completing on `bar` (bytes: multiple of 16, 16-byte aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+template <int N, int FK, int CG>
+__global__ void __launch_bounds__(256, (FxCfg<N, FK>::MINB)) fx_kernel(const FaceArgs a, const uint8_t* __restrict__ finfo,
+                                                                     const double* __restrict__ fcoef,
+                                                                     const __grid_constant__ FxMats<N> M) {
+  using C = FxCfg<N, FK>;
+  constexpr int N2 = C::N2, FPB = C::FPB, NT = C::NT, NP = C::NP, WP = C::WP, BAT = C::BAT, S = C::S;
+  constexpr int EPT = (FPB * N2 + NT - 1) / NT;  // epilogue values per thread
+  constexpr bool BLOCK = FK == FX_PREC || FK == FX_INIT || FK == FX_UPDATE;
+  constexpr bool RED = FK == FX_INIT || FK == FX_UPDATE;
+  constexpr bool POST = FK == FX_POST;
+  constexpr bool ODD = N & 1;  // row-wise stores N doubles apart are bank-conflict-free
+  if ((RED || (POST && CG)) && a.st->done) return;
+  extern __shared__ __align__(128) double smem[];
+  double* sStage = smem;                      // S x [OPS x BAT]: staged batches (G, then u)
+  double* sW = smem + S * C::OPS * BAT;       // exchange tile, FPB x WP
+  __shared__ __align__(8) uint64_t sBar[S];
+  __shared__ uint8_t sInf[FPB];
+  __shared__ double sCoef[FPB];
+  __shared__ double sWq[N];  // FX_POST: quadrature weights (dynamic index: keep out of the constant bank)
+  const int t = threadIdx.x, f = t / N, l = t - f * N;
+  if (POST && t < N) sWq[t] = M.B[t];
+  // FX_POST overwrites G (a.out) in place with r; a batch is staged before it is written
+  const double* src = POST ? a.out : a.in;
+  const int64_t nb = (a.nfaces + FPB - 1) / FPB;
+  const int64_t nmine = blockIdx.x < nb ? (nb - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // producer: batch k of this CTA -> stage k % S
+  auto issue = [&](int64_t k) {
+    const int64_t bt = blockIdx.x + k * gridDim.x;
+    const int64_t f0 = bt * FPB;
+    const int nf = (int)min((int64_t)FPB, a.nfaces - f0);
+    const uint32_t vals = (uint32_t)nf * N2, bulk = vals & ~1u;  // odd tail: one plain double
+    double* dst = sStage + (k % S) * C::OPS * BAT;
+    uint64_t* bar = &sBar[k % S];
+    if (bulk != vals) {  // before the arrive, whose release makes it visible to the waiters
+      dst[bulk] = src[f0 * N2 + bulk];
+      if (POST) dst[BAT + bulk] = a.in[f0 * N2 + bulk];
     }
-  }
-  const int64_t nb = (a.nfaces + FPC - 1) / FPC;
-  auto issue = [&](int64_t bt, double* dst) {
-    const int64_t f0 = bt * FPC;
-    const int nf = (int)min((int64_t)FPC, a.nfaces - f0);
-    const double* src = a.in + f0 * N2;
-    for (int it = threadIdx.x; it < nf * N2; it += blockDim.x) cp_async8f(dst + it, src + it);
+    mbar_expect_tx(bar, bulk * 8u * C::OPS);
+    bulk_g2s(dst, src + f0 * N2, bulk * 8u, bar);
+    if (POST) bulk_g2s(dst + BAT, a.in + f0 * N2, bulk * 8u, bar);
   };
-  int64_t bt = blockIdx.x;
-  if (bt < nb) issue(bt, sIn0);
-  asm volatile("cp.async.commit_group;\n" ::);
+  if (t == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&sBar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0)
+    for (int64_t k = 0; k < S - 1 && k < nmine; ++k) issue(k);
   double rz = 0.0;
-  int buf = 0;
-  for (; bt < nb; bt += gridDim.x, buf ^= 1) {
-    double* sIn = sIn0 + buf * V;
-    if (bt + gridDim.x < nb) issue(bt + gridDim.x, sIn0 + (buf ^ 1) * V);
-    asm volatile("cp.async.commit_group;\n" ::);
-    const int64_t f0 = bt * FPC;
-    const int nf = (int)min((int64_t)FPC, a.nfaces - f0);
-    if (threadIdx.x < nf) sInf[threadIdx.x] = finfo[f0 + threadIdx.x];
-    asm volatile("cp.async.wait_group 1;\n" ::);
-    __syncthreads();
-    // (A (x) A) X = A X A^T as two transposing row passes
-    rows_pass<N>(sA, sIn, nf, [&](int f, int j, int r, double v) { t1[f * N2 + j * N + r] = v; });
-    __syncthreads();
-    rows_pass<N>(sA, t1, nf, [&](int f, int j, int r, double v) {
-      const int q = j * N + r;
-      if (FK != BK_TRANSFORM) {  // * y^-1 (BlockPreconditioner, preconditioner.py:100-104)
-        v *= a.ycls ? __ldg(a.ycls + finfo_cls(sInf[f]) * N2 + q) : __ldg(a.yfull + (f0 + f) * N2 + q);
-      }
-      t2[f * N2 + q] = v;
-    });
-    __syncthreads();
-    if (FK != BK_TRANSFORM) {
-      rows_pass<N>(sB, t2, nf, [&](int f, int j, int r, double v) { t1[f * N2 + j * N + r] = v; });
-      __syncthreads();
-      rows_pass<N>(sB, t1, nf, [&](int f, int j, int r, double v) { t2[f * N2 + j * N + r] = v; });
-      __syncthreads();
+  for (int64_t k = 0; k < nmine; ++k) {
+    if (t == 0 && k + S - 1 < nmine) {
+      fence_proxy_async();  // the stage's previous generic reads happen before the async refill
+      issue(k + S - 1);
     }
-    for (int it = threadIdx.x; it < nf * N2; it += blockDim.x) {
+    const int64_t f0 = (blockIdx.x + k * gridDim.x) * FPB;
+    const int nf = (int)min((int64_t)FPB, a.nfaces - f0);
+    const bool on = f < nf;
+    if (t < nf) {
+      sInf[t] = finfo[f0 + t];
+      if (POST) sCoef[t] = fcoef[f0 + t];
+    }
+    double* sO = sStage + (k % S) * C::OPS * BAT;  // the stage, reused for the result once read
+    const double* sX = sO;
+    mbar_wait(&sBar[k % S], (uint32_t)(k / S) & 1u);
+    double x[N], y[N], z[N];
+    if (on) {  // pass 1 along the first index: column l
+      const double* xs = sX + f * N2 + l;
+#pragma unroll
+      for (int i = 0; i < N; ++i) x[i] = xs[i * N];
+      line_mv<N>(M.A, x, y);
+      double* ws = sW + f * WP + l;
+#pragma unroll
+      for (int j = 0; j < N; ++j) ws[j * NP] = y[j];
+    }
+    __syncthreads();
+    if (on) {  // pass 2 along the second index: row l
+      double* wr = sW + f * WP + l * NP;
+#pragma unroll
+      for (int c = 0; c < N; ++c) z[c] = wr[c];
+      line_mv<N>(M.A, z, y);
+      if (BLOCK) {  // * y^-1 (preconditioner.py:100-104), then pass 3 along the second index
+        const double* yi = a.ycls ? a.ycls + finfo_cls(sInf[f]) * N2 + l * N : a.yfull + (f0 + f) * N2 + l * N;
+#pragma unroll
+        for (int kk = 0; kk < N; ++kk) y[kk] *= __ldg(yi + kk);
+        line_mv<N>(M.B, y, z);
+#pragma unroll
+        for (int kk = 0; kk < N; ++kk) wr[kk] = z[kk];
+      } else if (ODD) {  // result row straight into the consumed stage, contiguous
+        double* orow = sO + f * N2 + l * N;
+#pragma unroll
+        for (int kk = 0; kk < N; ++kk) orow[kk] = y[kk];
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < N; ++kk) wr[kk] = y[kk];
+      }
+    }
+    if (BLOCK) {
+      __syncthreads();
+      if (on) {  // pass 4 along the first index: column l; <r, z> from the same column
+        double* wc = sW + f * WP + l;
+#pragma unroll
+        for (int j = 0; j < N; ++j) z[j] = wc[j * NP];
+        line_mv<N>(M.B, z, y);
+        const int kind = finfo_kind(sInf[f]);
+        if (kind == HDGB_DIRICHLET) {  // zero_dirichlet (preconditioner.py:107)
+#pragma unroll
+          for (int n = 0; n < N; ++n) y[n] = 0.0;
+        }
+        if (RED && kind_counts(kind)) {
+          double s = 0.0;
+#pragma unroll
+          for (int n = 0; n < N; ++n) s = fma(x[n], y[n], s);
+          rz += s;
+        }
+        if (ODD) {
+          double* ocol = sO + f * N2 + l;
+#pragma unroll
+          for (int n = 0; n < N; ++n) ocol[n * N] = y[n];
+        } else {
+#pragma unroll
+          for (int n = 0; n < N; ++n) wc[n * NP] = y[n];
+        }
+      }
+    }
+    __syncthreads();
+    // coalesced epilogue
+#pragma unroll
+    for (int m = 0; m < EPT; ++m) {
+      const int it = t + m * NT;
+      if (it >= nf * N2) break;
+      const int fi = it / N2, q = it - fi * N2, j = q / N, kk = q - j * N;
       const int64_t gi = f0 * N2 + it;
-      const int kind = finfo_kind(sInf[it / N2]);
-      double z = t2[it];
-      if (FK != BK_TRANSFORM && kind == HDGB_DIRICHLET) z = 0.0;  // zero_dirichlet (preconditioner.py:107)
-      a.out[gi] = z;
-      if (FK == BK_INIT) a.p[gi] = z;
-      if ((FK == BK_INIT || FK == BK_UPDATE) && kind_counts(kind)) rz = fma(sIn[it], z, rz);
+      // odd N: the result sits contiguous in the stage (conflict-free); even N: in the tile
+      double* wp = ODD ? sO + it : sW + fi * WP + j * NP + kk;
+      double v = *wp;
+      if (POST) {
+        // r = (sum_sides alpha_d GCC_ll) (w (x) w) u - (MS (x) MS) G
+        const double uv = sX[BAT + it];
+        v = ((sCoef[fi] * sWq[j]) * sWq[kk]) * uv - v;
+        if (CG) {
+          const int kind = finfo_kind(sInf[fi]);
+          if (kind == HDGB_DIRICHLET) v = 0.0;
+          sW[ODD ? it : fi * WP + j * NP + kk] = kind_counts(kind) ? uv * v : 0.0;
+        }
+      }
+      a.out[gi] = v;
+      if (FK == FX_INIT) a.p[gi] = v;
+    }
+    if (POST && CG) {  // per-face <u, r>, fixed order
+      __syncthreads();
+      const int lane = t & 31, warp = t >> 5, nw = NT >> 5;
+      for (int fi = warp; fi < nf; fi += nw) {
+        double acc = 0.0;
+        for (int q = lane; q < N2; q += 32) acc += sW[ODD ? fi * N2 + q : fi * WP + (q / N) * NP + q % N];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) a.facedot[f0 + fi] = acc;
+      }
     }
     __syncthreads();
   }
-  asm volatile("cp.async.wait_group 0;\n" ::);
-  if (FK == BK_INIT || FK == BK_UPDATE) {
+  if (RED) {
     double dummy = 0.0;
     block_sum2(rz, dummy);
     if (publish_last(a.part, rz, 0.0, &a.st->cnt[3])) {
       double trz, t0;
       final_sum2(a.part, gridDim.x, trz, t0);
       if (threadIdx.x == 0) {
-        if (FK == BK_INIT) cg_init_z(a.st, trz);
+        if (FK == FX_INIT) cg_init_z(a.st, trz);
         else cg_update_z(a.st, trz);
       }
     }
@@ -564,19 +697,65 @@ static cudaError_t pw_prec(hdgb_ctx* c, int prec, const FaceArgs& a, cudaStream_
   return cudaErrorInvalidValue;
 }
 
-template <int N, int FK>
-static cudaError_t blk_launch(hdgb_ctx* c, const FaceArgs& a, cudaStream_t s) {
-  using C = BlkCfg<N>;
+// Launch a face-block kernel with its 1D matrices (host copies, passed by value) on a grid
+// of at most one resident wave; the grid is fixed per device, so the reductions of the
+// CG variants are reproducible.
+template <int N, int FK, int CG = 0>
+static cudaError_t fx_launch(hdgb_ctx* c, const FaceArgs& a, const double* Ah, const double* Bh, int nb_b,
+                             cudaStream_t s) {
+  using C = FxCfg<N, FK>;
+  FxMats<N> M;
+  for (int q = 0; q < N * N; ++q) {
+    M.A[q] = Ah[q];
+    M.B[q] = q < nb_b ? Bh[q] : 0.0;
+  }
   const size_t smem = sizeof(double) * C::smem_doubles();
-  auto k = blk_kernel<N, FK>;
+  auto k = fx_kernel<N, FK, CG>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int64_t nb = (c->nfaces + C::FPC - 1) / C::FPC;
-  int grid = (int)min((int64_t)PW_GRID, nb);
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, C::NT, smem);
+  if (e != cudaSuccess) return e;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev);
+  const int64_t nb = (c->nfaces + C::FPB - 1) / C::FPB;
+  int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  if (grid > PW_GRID) grid = PW_GRID;
+  if (grid > nb) grid = nb;
   if (grid < 1) grid = 1;
-  k<<<grid, 256, smem, s>>>(a, c->d_finfo);
+  k<<<(unsigned)grid, C::NT, smem, s>>>(a, c->d_finfo, c->d_fcoef, M);
   c->launches++;
   return cudaGetLastError();
+}
+
+template <int N, int FK>
+static cudaError_t blk_launch(hdgb_ctx* c, const FaceArgs& a, cudaStream_t s) {
+  TabOff to;
+  to.set(N);
+  if (FK == FX_TRANSFORM) return fx_launch<N, FK>(c, a, a.A, nullptr, 0, s);
+  return fx_launch<N, FK>(c, a, c->h_tab.data() + to.St, c->h_tab.data() + to.S, N * N, s);
+}
+
+// plain-operator epilogue: r = coef (w (x) w) u - (MS (x) MS) G, in place over G = r
+cudaError_t launch_plain_post(hdgb_ctx* c, int cg, const double* u, double* r, cudaStream_t s) {
+  FaceArgs a = base_args(c, HDGB_PREC_NONE);
+  a.in = u;
+  a.out = r;
+  a.facedot = c->d_facedot;
+  TabOff to;
+  to.set(c->N);
+  const double* MS = c->h_tab.data() + to.MS;
+  const double* w = c->h_tab.data() + to.w;
+  switch (c->N) {
+#define HDGB_CASE(n)                                                             \
+  case n:                                                                        \
+    return cg ? fx_launch<n, FX_POST, 1>(c, a, MS, w, n, s) : fx_launch<n, FX_POST, 0>(c, a, MS, w, n, s);
+    HDGB_CASE(2) HDGB_CASE(3) HDGB_CASE(4) HDGB_CASE(5) HDGB_CASE(6) HDGB_CASE(7) HDGB_CASE(8) HDGB_CASE(9)
+    HDGB_CASE(10) HDGB_CASE(11) HDGB_CASE(12) HDGB_CASE(13) HDGB_CASE(14) HDGB_CASE(15) HDGB_CASE(16)
+    HDGB_CASE(17)
+#undef HDGB_CASE
+  }
+  return cudaErrorInvalidValue;
 }
 
 enum { OP_PREC = 0, OP_TRANSFORM = 1, OP_CG_INIT = 2, OP_CG_UPDATE = 3 };
@@ -586,16 +765,16 @@ static cudaError_t face_n(hdgb_ctx* c, int op, int prec, const FaceArgs& a, cuda
   cudaError_t e;
   switch (op) {
     case OP_TRANSFORM:
-      return blk_launch<N, BK_TRANSFORM>(c, a, s);
+      return blk_launch<N, FX_TRANSFORM>(c, a, s);
     case OP_PREC:
-      if (prec == HDGB_PREC_BLOCK) return blk_launch<N, BK_PREC>(c, a, s);
+      if (prec == HDGB_PREC_BLOCK) return blk_launch<N, FX_PREC>(c, a, s);
       return pw_prec<N, PW_PREC, true>(c, prec, a, s);
     case OP_CG_INIT:
       if ((e = pw_prec<N, PW_INIT, true>(c, prec, a, s)) != cudaSuccess) return e;
       if (prec == HDGB_PREC_BLOCK) {
         FaceArgs b = a;
         b.in = a.r;  // z = P r, p = z, <r,z>
-        return blk_launch<N, BK_INIT>(c, b, s);
+        return blk_launch<N, FX_INIT>(c, b, s);
       }
       return cudaSuccess;
     case OP_CG_UPDATE:
@@ -603,7 +782,7 @@ static cudaError_t face_n(hdgb_ctx* c, int op, int prec, const FaceArgs& a, cuda
       if (prec == HDGB_PREC_BLOCK) {
         FaceArgs b = a;
         b.in = a.r;
-        return blk_launch<N, BK_UPDATE>(c, b, s);
+        return blk_launch<N, FX_UPDATE>(c, b, s);
       }
       return cudaSuccess;
   }
@@ -623,9 +802,9 @@ static cudaError_t face_any(hdgb_ctx* c, int op, int prec, const FaceArgs& a, cu
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_face_transform(hdgb_ctx* c, const double* A_dev, const double* in, double* out, cudaStream_t s) {
+cudaError_t launch_face_transform(hdgb_ctx* c, const double* A_host, const double* in, double* out, cudaStream_t s) {
   FaceArgs a = base_args(c, HDGB_PREC_NONE);
-  a.A = A_dev;
+  a.A = A_host;
   a.in = in;
   a.out = out;
   return face_any(c, OP_TRANSFORM, HDGB_PREC_NONE, a, s);

@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/hdgb.h"
 
@@ -99,9 +100,6 @@ struct OpArgs {
   Geo g;
   const double* u;
   double* r;
-  double* xbuf;
-  int64_t xstride;
-  uint32_t* tickets;
   double* facedot;
   const double* tab;
   const double* dz;      // N^3 shared table (uniform) or nullptr
@@ -123,7 +121,7 @@ struct FaceArgs {
   const double* in;
   double* out;
   // generic transform
-  const double* A;       // device N*N (transform kernel)
+  const double* A;       // host N*N (transform launcher; passed to the kernel by value)
   // CG fused update
   double* x;
   double* p;
@@ -131,6 +129,7 @@ struct FaceArgs {
   const double* w;
   double* z;
   double* part;          // per-CTA partials [gridDim][2]
+  double* facedot;       // per-face <u, r> (plain epilogue, CG mode)
   CGState* st;
 };
 
@@ -245,7 +244,6 @@ struct hdgb_ctx {
   int uniform;
   double al_u[4];
   int64_t n_all, n_unknown, nfaces;
-  int64_t xstride;
   double* d_tab = nullptr;
   double* d_dz = nullptr;
   double* d_widths = nullptr;
@@ -255,12 +253,12 @@ struct hdgb_ctx {
   double* d_yinv_full = nullptr;  // non-uniform variants (n_all each)
   double* d_y_full = nullptr;
   double* d_dn_full = nullptr;
-  double* d_xbuf = nullptr;
-  uint32_t* d_tickets = nullptr;
   uint8_t* d_finfo = nullptr;     // per-face kind/class byte
   double* d_facedot = nullptr;
   double* d_part = nullptr;
-  double* d_A = nullptr;          // transform matrix scratch N*N
+  std::vector<double> h_tab;      // host copy of d_tab (1D matrices become kernel parameters)
+  double* d_fcoef = nullptr;      // per-face self-term coefficient sum_sides alpha_d GCC_ll
+  double* d_hat = nullptr;        // plain operator: eigen-space input (T (x) T) u  (n_all)
   hdgb::CGState* d_st = nullptr;
   hdgb::CGState* h_st = nullptr;  // pinned mirror
   double* d_vec = nullptr;        // CG vectors x r z p w F (6 * n_all)
@@ -283,7 +281,8 @@ int cuda_fail(cudaError_t e, const char* what);
 
 // launchers (defined per translation unit)
 cudaError_t launch_op(hdgb_ctx* c, int variant, int mode, const double* u, double* r, cudaStream_t s);
-cudaError_t launch_face_transform(hdgb_ctx* c, const double* A_dev, const double* in, double* out, cudaStream_t s);
+cudaError_t launch_face_transform(hdgb_ctx* c, const double* A_host, const double* in, double* out, cudaStream_t s);
+cudaError_t launch_plain_post(hdgb_ctx* c, int cg, const double* u, double* r, cudaStream_t s);
 cudaError_t launch_prec(hdgb_ctx* c, int kind, const double* in, double* out, cudaStream_t s);
 cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s);
 cudaError_t launch_cg_init(hdgb_ctx* c, int kind, cudaStream_t s);

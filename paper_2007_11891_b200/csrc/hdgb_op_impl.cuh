@@ -567,7 +567,8 @@ __global__ void __launch_bounds__(OpTCfg<N>::W(COLOR) * 32) opT_kernel(OpArgs a,
     __syncwarp();
     // contribution c = alpha_d GCC_ll u - g (+ colour-0 partial `prev`) stored to r (operator.py:243-257)
     auto emit = [&](int s, int q, double gval, double uval, double prev) {
-      double val = cf[s] * uval - gval;
+      // GONLY (plain core): the eigen-space face sum of g only; the face epilogue adds the rest
+      double val = (MODE & 4) ? gval : cf[s] * uval - gval;
       if (COLOR == 1 && sh[s]) val = prev + val;
       if ((MODE & 1) && (COLOR == 1 || !sh[s])) {
         if (kinds[s] == HDGB_DIRICHLET) val = 0.0;
@@ -715,19 +716,27 @@ static cudaError_t launch_passT(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
 
 template <int N, bool PLAIN, int MODE, int COLOR>
 static cudaError_t launch_any(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_t t1, cudaStream_t s) {
-  if (PLAIN) return launch_pass<N, PLAIN, MODE, COLOR>(c, a, t0, t1, s);
+  if (PLAIN) return launch_passT<N, (MODE & ~1) | 4, COLOR>(c, a, t0, t1, s);  // dots: epilogue
   return launch_passT<N, MODE, COLOR>(c, a, t0, t1, s);
 }
 
+// Alg. 2 (plain) = (MS (x) MS) [transformed core without self term] (T (x) T) + self term:
+// the tangential transforms act per face, so they commute with the face sum of the two
+// element contributions and run once per face instead of once per element side.
 template <int N, bool PLAIN, int MODE>
 static cudaError_t launch_t(hdgb_ctx* c, const double* u, double* r, cudaStream_t s) {
   OpArgs a;
   a.g = c->g;
   a.u = u;
   a.r = r;
-  a.xbuf = c->d_xbuf;
-  a.xstride = c->xstride;
-  a.tickets = c->d_tickets;
+  if (PLAIN) {
+    if (c->g.ne == 0) return cudaSuccess;
+    TabOff to;
+    to.set(N);
+    cudaError_t e = launch_face_transform(c, c->h_tab.data() + to.T, u, c->d_hat, s);
+    if (e != cudaSuccess) return e;
+    a.u = c->d_hat;
+  }
   a.facedot = c->d_facedot;
   a.tab = c->d_tab;
   a.dz = c->d_dz;
@@ -761,6 +770,7 @@ static cudaError_t launch_t(hdgb_ctx* c, const double* u, double* r, cudaStream_
       if (e != cudaSuccess) return e;
     }
   }
+  if (PLAIN) return launch_plain_post(c, MODE & 1, u, r, s);
   return cudaSuccess;
 }
 
