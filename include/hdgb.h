@@ -77,7 +77,9 @@ int64_t hdgb_ctx_n_unknown(const hdgb_ctx* ctx);  /* mesh.n_trace_unknowns(p)   
 int64_t hdgb_ctx_n_faces(const hdgb_ctx* ctx, int d);
 
 /* r = K u on all faces (hdg_op_3d, operator.py:261-267 / hdg_op_3d_transformed 270-276).
- * u and r must not alias.  Dirichlet rows are evaluated like the reference. */
+ * u and r must not alias.  Dirichlet rows are evaluated like the reference.
+ * Device vectors passed to hdgb_op_apply / hdgb_face_transform / hdgb_prec_apply must be
+ * 16-byte aligned (cudaMalloc and torch allocations are); HDGB_EINVAL otherwise. */
 int hdgb_op_apply(hdgb_ctx* ctx, int variant, const double* u, double* r, void* stream);
 
 /* Same with HOST buffers (pinned for full PCIe speed): copies in, applies, copies out,

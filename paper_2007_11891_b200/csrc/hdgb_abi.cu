@@ -31,6 +31,8 @@ static int einval(const std::string& m) {
   return HDGB_EINVAL;
 }
 enum { V_X = 0, V_R = 1, V_Z = 2, V_P = 3, V_W = 4, V_F = 5 };
+// the face-block kernels stream vectors with 16-byte bulk copies
+static bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 }  // namespace hdgb
 
 using namespace hdgb;
@@ -103,6 +105,7 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
   for (int q = 0; q < 6; ++q) g.kind[q] = d->side_kind[q];
   c->nfaces = g.nf[0] + g.nf[1] + g.nf[2];
   c->n_all = c->nfaces * N2;
+  c->vstride = (c->n_all + 31) / 32 * 32;  // 256-byte aligned vector slots
   int64_t unk = 0;
   for (int q = 0; q < 3; ++q) {
     int nd = q == 0 ? g.n1 : (q == 1 ? g.n2 : g.n3);
@@ -281,6 +284,7 @@ int hdgb_op_apply(hdgb_ctx* c, int variant, const double* u, double* r, void* st
   if (!c || !u || !r) return einval("null argument");
   if (variant != HDGB_PLAIN && variant != HDGB_TRANSFORMED) return einval("unknown operator variant");
   if (u == r) return einval("input and output must not alias");
+  if (!al16(u) || !al16(r)) return einval("device vectors must be 16-byte aligned");
   HDGB_CUDA(launch_op(c, variant, MODE_APPLY, u, r, (cudaStream_t)stream));
   return HDGB_OK;
 }
@@ -289,11 +293,11 @@ int hdgb_op_apply_host(hdgb_ctx* c, int variant, const double* u_host, double* r
   if (!c || !u_host || !r_host) return einval("null argument");
   if (variant != HDGB_PLAIN && variant != HDGB_TRANSFORMED) return einval("unknown operator variant");
   cudaStream_t s = (cudaStream_t)stream;
-  if (!c->d_io) HDGB_CUDA(cudaMalloc(&c->d_io, sizeof(double) * 2 * c->n_all));
+  if (!c->d_io) HDGB_CUDA(cudaMalloc(&c->d_io, sizeof(double) * 2 * c->vstride));
   const size_t bytes = sizeof(double) * c->n_all;
   HDGB_CUDA(cudaMemcpyAsync(c->d_io, u_host, bytes, cudaMemcpyHostToDevice, s));
-  HDGB_CUDA(launch_op(c, variant, MODE_APPLY, c->d_io, c->d_io + c->n_all, s));
-  HDGB_CUDA(cudaMemcpyAsync(r_host, c->d_io + c->n_all, bytes, cudaMemcpyDeviceToHost, s));
+  HDGB_CUDA(launch_op(c, variant, MODE_APPLY, c->d_io, c->d_io + c->vstride, s));
+  HDGB_CUDA(cudaMemcpyAsync(r_host, c->d_io + c->vstride, bytes, cudaMemcpyDeviceToHost, s));
   HDGB_CUDA(cudaStreamSynchronize(s));
   return HDGB_OK;
 }
@@ -301,8 +305,9 @@ int hdgb_op_apply_host(hdgb_ctx* c, int variant, const double* u_host, double* r
 int hdgb_face_transform(hdgb_ctx* c, const double* A_host, const double* in, double* out, void* stream) {
   if (!c || !A_host || !in || !out) return einval("null argument");
   if (in == out) return einval("input and output must not alias");
+  if (!al16(in) || !al16(out)) return einval("device vectors must be 16-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
-  // stage A through the ctx (pageable copy is synchronous w.r.t. the host)
+  // A travels by value as a kernel parameter
   HDGB_CUDA(launch_face_transform(c, A_host, in, out, s));
   return HDGB_OK;
 }
@@ -310,6 +315,7 @@ int hdgb_face_transform(hdgb_ctx* c, const double* A_host, const double* in, dou
 int hdgb_prec_apply(hdgb_ctx* c, int kind, const double* r, double* z, void* stream) {
   if (!c || !r || !z) return einval("null argument");
   if (kind < HDGB_PREC_NONE || kind > HDGB_PREC_DIAG_EIGEN) return einval("unknown preconditioner kind");
+  if (!al16(r) || !al16(z)) return einval("device vectors must be 16-byte aligned");
   HDGB_CUDA(launch_prec(c, kind, r, z, (cudaStream_t)stream));
   return HDGB_OK;
 }
@@ -392,7 +398,7 @@ static cudaError_t enqueue_iteration(hdgb_ctx* c, int variant, int prec, cudaGra
   double* v = c->d_vec;
   const int64_t n = c->n_all;
   cudaError_t e;
-  if ((e = launch_op(c, variant, MODE_CG, v + V_P * n, v + V_W * n, c->s)) != cudaSuccess) return e;  // w = K p, <p,w>
+  if ((e = launch_op(c, variant, MODE_CG, v + V_P * c->vstride, v + V_W * c->vstride, c->s)) != cudaSuccess) return e;  // w = K p, <p,w>
   if ((e = launch_reduce_pw(c, c->s)) != cudaSuccess) return e;                                      // alpha
   if ((e = launch_cg_update(c, prec, c->s)) != cudaSuccess) return e;  // x,r update; z = P r; ||r||, <r,z>
   return launch_p_update(c, c->s, h, has_loop);                        // p = z + beta p; loop control
@@ -450,14 +456,14 @@ int hdgb_pcg(hdgb_ctx* c, int variant, int prec, const double* F, double* x, dou
   cudaStream_t us = (cudaStream_t)stream;
   const int64_t n = c->n_all;
   const size_t bytes = sizeof(double) * n;
-  if (!c->d_vec) HDGB_CUDA(cudaMalloc(&c->d_vec, 6 * bytes));
+  if (!c->d_vec) HDGB_CUDA(cudaMalloc(&c->d_vec, sizeof(double) * 6 * c->vstride));
   double* v = c->d_vec;
   // order after the caller's stream
   HDGB_CUDA(cudaEventRecord(c->ev_in, us));
   HDGB_CUDA(cudaStreamWaitEvent(c->s, c->ev_in, 0));
-  HDGB_CUDA(cudaMemcpyAsync(v + V_F * n, F, bytes, cudaMemcpyDeviceToDevice, c->s));
-  HDGB_CUDA(cudaMemcpyAsync(v + V_X * n, x, bytes, cudaMemcpyDeviceToDevice, c->s));
-  HDGB_CUDA(launch_pack(c, 2, v + V_X * n, v + V_X * n, c->s));  // unknowns only (unpack_unknowns)
+  HDGB_CUDA(cudaMemcpyAsync(v + V_F * c->vstride, F, bytes, cudaMemcpyDeviceToDevice, c->s));
+  HDGB_CUDA(cudaMemcpyAsync(v + V_X * c->vstride, x, bytes, cudaMemcpyDeviceToDevice, c->s));
+  HDGB_CUDA(launch_pack(c, 2, v + V_X * c->vstride, v + V_X * c->vstride, c->s));  // unknowns only (unpack_unknowns)
   CGState* h = c->h_st;
   memset(h, 0, sizeof(CGState));
   h->rtol = rtol;
@@ -465,7 +471,7 @@ int hdgb_pcg(hdgb_ctx* c, int variant, int prec, const double* F, double* x, dou
   h->max_iters = max_iters;
   HDGB_CUDA(cudaMemcpyAsync(c->d_st, h, sizeof(CGState), cudaMemcpyHostToDevice, c->s));
   // r = F - K x0; z = P r; p = z; norm0, rho (solver.py:290-302)
-  HDGB_CUDA(launch_op(c, variant, MODE_APPLY, v + V_X * n, v + V_W * n, c->s));
+  HDGB_CUDA(launch_op(c, variant, MODE_APPLY, v + V_X * c->vstride, v + V_W * c->vstride, c->s));
   HDGB_CUDA(launch_cg_init(c, prec, c->s));
   HDGB_CUDA(cudaMemcpyAsync(h, c->d_st, sizeof(CGState), cudaMemcpyDeviceToHost, c->s));
   HDGB_CUDA(cudaStreamSynchronize(c->s));
@@ -497,7 +503,7 @@ int hdgb_pcg(hdgb_ctx* c, int variant, int prec, const double* F, double* x, dou
     HDGB_CUDA(cudaStreamSynchronize(c->s));
     if (use_graph) c->launches += 4LL * (h->it > 0 ? h->it - 1 : 0);
   }
-  HDGB_CUDA(cudaMemcpyAsync(x, v + V_X * n, bytes, cudaMemcpyDeviceToDevice, c->s));
+  HDGB_CUDA(cudaMemcpyAsync(x, v + V_X * c->vstride, bytes, cudaMemcpyDeviceToDevice, c->s));
   HDGB_CUDA(cudaEventRecord(c->ev_out, c->s));
   HDGB_CUDA(cudaStreamWaitEvent(us, c->ev_out, 0));
   *iters = h->it;

@@ -841,11 +841,11 @@ cudaError_t launch_cg_init(hdgb_ctx* c, int kind, cudaStream_t s) {
   FaceArgs a = base_args(c, kind);
   double* v = c->d_vec;
   const int64_t n = c->n_all;
-  a.in = v + V_F * n;
-  a.w = v + V_W * n;
-  a.r = v + V_R * n;
-  a.out = v + V_Z * n;
-  a.p = v + V_P * n;
+  a.in = v + V_F * c->vstride;
+  a.w = v + V_W * c->vstride;
+  a.r = v + V_R * c->vstride;
+  a.out = v + V_Z * c->vstride;
+  a.p = v + V_P * c->vstride;
   return face_any(c, OP_CG_INIT, kind, a, s);
 }
 
@@ -853,11 +853,11 @@ cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s) {
   FaceArgs a = base_args(c, kind);
   double* v = c->d_vec;
   const int64_t n = c->n_all;
-  a.x = v + V_X * n;
-  a.p = v + V_P * n;
-  a.r = v + V_R * n;
-  a.w = v + V_W * n;
-  a.out = v + V_Z * n;
+  a.x = v + V_X * c->vstride;
+  a.p = v + V_P * c->vstride;
+  a.r = v + V_R * c->vstride;
+  a.w = v + V_W * c->vstride;
+  a.out = v + V_Z * c->vstride;
   return face_any(c, OP_CG_UPDATE, kind, a, s);
 }
 
@@ -871,7 +871,7 @@ cudaError_t launch_reduce_pw(hdgb_ctx* c, cudaStream_t s) {
 cudaError_t launch_p_update(hdgb_ctx* c, cudaStream_t s, cudaGraphConditionalHandle loop, int has_loop) {
   double* v = c->d_vec;
   const int64_t n = c->n_all;
-  p_update_kernel<<<grid_for(n, 1024), 1024, 0, s>>>(v + V_Z * n, v + V_P * n, n, c->d_st, loop, has_loop);
+  p_update_kernel<<<grid_for(n, 1024), 1024, 0, s>>>(v + V_Z * c->vstride, v + V_P * c->vstride, n, c->d_st, loop, has_loop);
   c->launches++;
   return cudaGetLastError();
 }

@@ -244,6 +244,7 @@ struct hdgb_ctx {
   int uniform;
   double al_u[4];
   int64_t n_all, n_unknown, nfaces;
+  int64_t vstride;  // slot stride of the CG / staging vectors (n_all rounded up to 32)
   double* d_tab = nullptr;
   double* d_dz = nullptr;
   double* d_widths = nullptr;

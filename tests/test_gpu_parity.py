@@ -273,3 +273,33 @@ def test_fused_pcg_zero_rhs():
     F = np.zeros(mesh.n_trace_unknowns(ctx.basis.p))
     x, it, rel, conv = hb.pcg(hb.DeviceOperator(ctx, 0), hb.build_block_preconditioner(ctx).apply_packed, F, F)
     assert conv and it == 0 and rel == 0.0 and not np.any(x)
+
+
+def test_odd_length_vectors_and_alignment():
+    """n_all odd (11 faces x 25 values): bulk-copy tails and padded CG slots; misaligned
+    device vectors are rejected (the face-block kernels stream 16-byte bulk copies)."""
+    bc = ("neumann", "dirichlet", "neumann", "neumann", "dirichlet", "neumann")
+    p, lo, hi = 4, (0.0, 0.0, 0.0), (2.0, 1.0, 1.0)
+    mesh = hb.Mesh((2, 1, 1), lo, hi, bc)
+    assert mesh.n_all(p) % 2 == 1
+    ctx = hb.OperatorContext(hb.Basis1D(p, 0.8), mesh, 0.3)
+    octx = O.context(O.basis_1d(p, 0.8), O.Grid.uniform(mesh.n, lo, hi, bc), 0.3)
+    rng = np.random.default_rng(11)
+    u = rng.uniform(-1, 1, mesh.n_all(p))
+    dc = hb.device_context(ctx)
+    for variant, tr in ((0, False), (1, True)):
+        assert relerr(dc.apply(_dev(u), variant).cpu().numpy(), O.apply_op(octx, u, tr)) < TOL
+    y = O.face_selfcoupling(octx)
+    assert relerr(dc.prec(_dev(u), 1).cpu().numpy(), O.block_prec_apply(octx, y, u)) < TOL
+    F = rng.uniform(-1, 1, mesh.n_trace_unknowns(p))
+    x, it, rel, conv = hb.pcg(hb.DeviceOperator(ctx, 0), hb.build_block_preconditioner(ctx).apply_packed, F,
+                              np.zeros_like(F), rtol=1e-10)
+    grid, n = octx["grid"], octx["n"]
+    xo, ito, _, _ = O.pcg(lambda v: O.apply_op_packed(octx, v),
+                          lambda r: O.pack(grid, n, O.block_prec_apply(octx, y, O.unpack(grid, n, r))), F,
+                          np.zeros_like(F))
+    assert conv and abs(it - ito) <= 1
+    assert relerr(x, xo) < 1e-9
+    buf = torch.zeros(mesh.n_all(p) + 1, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError, match="aligned"):
+        dc.apply(buf[1:], 0)
