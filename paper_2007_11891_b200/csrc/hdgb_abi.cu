@@ -106,6 +106,10 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
   c->nfaces = g.nf[0] + g.nf[1] + g.nf[2];
   c->n_all = c->nfaces * N2;
   c->vstride = (c->n_all + 31) / 32 * 32;  // 256-byte aligned vector slots
+  if (c->n_all + 32 >= (int64_t)1 << 32) {
+    delete c;
+    return einval("at most 2^32 - 33 trace values per device (partition the grid across GPUs)");
+  }
   int64_t unk = 0;
   for (int q = 0; q < 3; ++q) {
     int nd = q == 0 ? g.n1 : (q == 1 ? g.n2 : g.n3);

@@ -102,6 +102,9 @@ struct OpVCfg {
   static constexpr int NQ = N * N;                      // threads (face positions) per element
   static constexpr int G = NQ >= 256 ? 1 : 256 / NQ;    // elements per CTA
   static constexpr int NT = (G * NQ + 31) / 32 * 32;    // threads per CTA
+  // register budget: 3 CTAs of 256 threads per SM (85 registers); the 1D tables stay in the
+  // constant bank instead of being hoisted into registers
+  static constexpr int MINB = NT > 256 ? 2 : (NT > 192 ? 3 : 4);
   static constexpr int FS = 6 * NQ;                     // staged faces of one element
   static constexpr int VS = N * NQ;                     // U volume of one element
   __host__ __device__ static constexpr int smem_doubles(bool cg) { return G * (2 * FS + VS + (cg ? FS : 0)); }
@@ -117,6 +120,7 @@ struct OpVConst {
 // per element slot, written by one thread per group
 struct ElemInfo {
   long long fid[6];
+  unsigned off[6];  // fid * N^2: 32-bit element offsets (n_all < 2^32, checked at create)
   double al[4];
   int valid;
   unsigned shared;
@@ -126,7 +130,7 @@ struct ElemInfo {
 // MODE bit 0: CG (Dirichlet rows -> 0, per-face <u, r>); bit 1: non-uniform grid (per-element
 // metric terms and dz_inv); bit 2: "g only" (plain core: emit the eigen-space sum of g only).
 template <int N, int MODE, int COLOR>
-__global__ void __launch_bounds__(OpVCfg<N>::NT) opV_kernel(const OpArgs a, int64_t t0, int64_t t1,
+__global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(const OpArgs a, int64_t t0, int64_t t1,
                                                           const __grid_constant__ OpVConst<N> K) {
   using C = OpVCfg<N>;
   constexpr int NQ = C::NQ, G = C::G, FS = C::FS, VS = C::VS;
@@ -168,6 +172,7 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT) opV_kernel(const OpArgs a, int6
 #pragma unroll
         for (int s = 0; s < 6; ++s) {
           I.fid[s] = E.fid[s];
+          I.off[s] = (unsigned)E.fid[s] * (unsigned)NQ;
           I.kind[s] = face_kind(g, s >> 1, E.c[s >> 1] + (s & 1));
         }
 #pragma unroll
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT) opV_kernel(const OpArgs a, int6
     if (act && inf[e].valid) {
       double* dst = buf + e * FS + q;
 #pragma unroll
-      for (int s = 0; s < 6; ++s) cp_async8(dst + s * NQ, a.u + inf[e].fid[s] * NQ + q);
+      for (int s = 0; s < 6; ++s) cp_async8(dst + s * NQ, a.u + (inf[e].off[s] + (unsigned)q));
     }
   };
 
@@ -206,7 +211,7 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT) opV_kernel(const OpArgs a, int6
     double prev[6];
     if (COLOR == 1 && on) {
 #pragma unroll
-      for (int s = 0; s < 6; ++s) prev[s] = (I.shared >> s & 1u) ? __ldcg(a.r + I.fid[s] * NQ + q) : 0.0;
+      for (int s = 0; s < 6; ++s) prev[s] = (I.shared >> s & 1u) ? __ldcg(a.r + (I.off[s] + (unsigned)q)) : 0.0;
     }
     // contribution alpha_d GCC_ll u - g (operator.py:243-257) at position q of face s;
     // ua = alpha_d u, ur = u
@@ -219,7 +224,7 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT) opV_kernel(const OpArgs a, int6
         if (fin && I.kind[s] == HDGB_DIRICHLET) val = 0.0;
         dotp[s * NQ + q] = (fin && kind_counts(I.kind[s])) ? ur * val : 0.0;
       }
-      a.r[I.fid[s] * NQ + q] = val;
+      a.r[I.off[s] + (unsigned)q] = val;
     };
     if (on) {  // phase 1: x-line of (a2, a3) = (qa, qb)
       const double al1 = I.al[1], al2 = I.al[2], al3 = I.al[3];
@@ -292,6 +297,8 @@ static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
   const size_t smem = sizeof(double) * (size_t)Cf::smem_doubles(MODE & 1);
   auto kern = opV_kernel<N, MODE, COLOR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cf::NT, smem);
