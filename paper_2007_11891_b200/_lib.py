@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_hdgb.so")
+LIB_PATH = os.environ.get("HDGB_LIB") or os.path.join(_HERE, "_hdgb.so")  # HDGB_LIB: tuning side builds
 
 OK, EINVAL, EBREAKDOWN, ECUDA, ENCCL, ENONFINITE = 0, 1, 2, 3, 4, 5
 INTERIOR, DIRICHLET, NEUMANN, HALO_OWNED, HALO_PEER = 0, 1, 2, 3, 4

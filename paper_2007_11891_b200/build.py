@@ -15,8 +15,11 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(ROOT, "build")
-OUT = os.path.join(HERE, "_hdgb.so")
+# HDGB_BUILD_TAG / HDGB_DEFS: side builds for tuning experiments (build_<tag>/, _hdgb_<tag>.so,
+# extra -D definitions); the product build uses neither
+_TAG = os.environ.get("HDGB_BUILD_TAG", "")
+BUILD = os.path.join(ROOT, "build" + (f"_{_TAG}" if _TAG else ""))
+OUT = os.path.join(HERE, f"_hdgb_{_TAG}.so" if _TAG else "_hdgb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
@@ -39,7 +42,7 @@ def up_to_date():
 
 def _compile(src):
     obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *os.environ.get("HDGB_DEFS", "").split(), "-c", src, "-o", obj]
     if os.environ.get("HDGB_PTXAS_VERBOSE"):
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -102,9 +102,12 @@ struct OpVCfg {
   static constexpr int NQ = N * N;                      // threads (face positions) per element
   static constexpr int G = NQ >= 256 ? 1 : 256 / NQ;    // elements per CTA
   static constexpr int NT = (G * NQ + 31) / 32 * 32;    // threads per CTA
-  // register budget: 3 CTAs of 256 threads per SM (85 registers); the 1D tables stay in the
-  // constant bank instead of being hoisted into registers
-  static constexpr int MINB = NT > 256 ? 2 : (NT > 192 ? 3 : 4);
+#ifdef HDGB_OPV_MINB
+  static constexpr int MINB = HDGB_OPV_MINB;
+#else
+  // register budget (CTAs per SM): measured on the config-3 sweep (p = 2..16)
+  static constexpr int MINB = NT > 256 ? 2 : (N <= 7 ? 3 : (N <= 11 ? 2 : 3));
+#endif
   static constexpr int FS = 6 * NQ;                     // staged faces of one element
   static constexpr int VS = N * NQ;                     // U volume of one element
   __host__ __device__ static constexpr int smem_doubles(bool cg) { return G * (2 * FS + VS + (cg ? FS : 0)); }
@@ -202,8 +205,18 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
     cp_async_commit();
     asm volatile("cp.async.wait_group 1;\n" ::);
     __syncthreads();
+    // element geometry into registers once
     const ElemInfo& I = sInfo[buf][act ? e : 0];
     const bool on = act && I.valid;
+    unsigned off[6];
+    int kinds[6];
+#pragma unroll
+    for (int s2 = 0; s2 < 6; ++s2) {
+      off[s2] = I.off[s2] + (unsigned)q;
+      kinds[s2] = CG ? I.kind[s2] : 0;
+    }
+    const unsigned shared = I.shared;
+    const double al0 = I.al[0], al1 = I.al[1], al2 = I.al[2], al3 = I.al[3];
     const double* sF = sF0 + buf * G * FS + (act ? e : 0) * FS;
     double* vU = sU + (act ? e : 0) * VS;
     double* dotp = sDot + (act ? e : 0) * FS;
@@ -211,27 +224,26 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
     double prev[6];
     if (COLOR == 1 && on) {
 #pragma unroll
-      for (int s = 0; s < 6; ++s) prev[s] = (I.shared >> s & 1u) ? __ldcg(a.r + (I.off[s] + (unsigned)q)) : 0.0;
+      for (int s = 0; s < 6; ++s) prev[s] = (shared >> s & 1u) ? __ldcg(a.r + off[s]) : 0.0;
     }
     // contribution alpha_d GCC_ll u - g (operator.py:243-257) at position q of face s;
     // ua = alpha_d u, ur = u
     auto emit = [&](int s, double gval, double ua, double ur) {
-      const bool sh = I.shared >> s & 1u;
+      const bool sh = shared >> s & 1u;
       double val = GONLY ? gval : ((s & 1) ? gcc1 : gcc0) * ua - gval;
       if (COLOR == 1 && sh) val = prev[s] + val;
       const bool fin = COLOR == 1 || !sh;
       if (CG) {
-        if (fin && I.kind[s] == HDGB_DIRICHLET) val = 0.0;
-        dotp[s * NQ + q] = (fin && kind_counts(I.kind[s])) ? ur * val : 0.0;
+        if (fin && kinds[s] == HDGB_DIRICHLET) val = 0.0;
+        dotp[s * NQ + q] = (fin && kind_counts(kinds[s])) ? ur * val : 0.0;
       }
-      a.r[I.off[s] + (unsigned)q] = val;
+      a.r[off[s]] = val;
     };
     if (on) {  // phase 1: x-line of (a2, a3) = (qa, qb)
-      const double al1 = I.al[1], al2 = I.al[2], al3 = I.al[3];
       const double xr0 = sF[q], xr1 = sF[NQ + q];
       const double x0 = al1 * xr0, x1 = al1 * xr1;
       const double by0 = al2 * b0a, by1 = al2 * b1a, bz0 = al3 * b0b, bz1 = al3 * b1b;
-      const double base = UNI ? 0.0 : a.lam * I.al[0] + al2 * lama + al3 * lamb;
+      const double base = UNI ? 0.0 : a.lam * al0 + al2 * lama + al3 * lamb;
       double ax0 = 0.0, ax1 = 0.0;
 #pragma unroll
       for (int a1 = 0; a1 < N; ++a1) {
@@ -265,7 +277,6 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
         az0 = fma(K.B0[k], vz, az0);
         az1 = fma(K.B1[k], vz, az1);
       }
-      const double al2 = I.al[2], al3 = I.al[3];
       const double yr0 = sF[2 * NQ + q], yr1 = sF[3 * NQ + q], zr0 = sF[4 * NQ + q], zr1 = sF[5 * NQ + q];
       emit(2, al2 * ay0, al2 * yr0, yr0);
       emit(3, al2 * ay1, al2 * yr1, yr1);
@@ -297,8 +308,6 @@ static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
   const size_t smem = sizeof(double) * (size_t)Cf::smem_doubles(MODE & 1);
   auto kern = opV_kernel<N, MODE, COLOR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cf::NT, smem);
