@@ -119,35 +119,59 @@ __global__ void __launch_bounds__(256) pw_kernel(FaceArgs a, const uint8_t* __re
 // ================================================================ face-block kernels
 // Every face block is an N x N tile X (rows = first tangential index).  The kernels apply
 // tensor-product operators (A (x) A) X = A X A^T and the block preconditioner
-// (S (x) S) y^-1 (S^T (x) S^T) (preconditioner.py:96-110) as 1D line passes:
-//  * batches of FPB faces are contiguous in HBM: one elected thread streams them into a
-//    ring of shared-memory stages with bulk async copies (cp.async.bulk + mbarrier
-//    transaction counts), S-1 batches ahead, so the loads cost no issue slots and keep
-//    tens of KB per SM in flight;
-//  * one thread per (face, line): a pass along the first index works on a COLUMN held in
-//    registers, a pass along the second index on a ROW; the four passes of Alg. 4 need only
-//    two exchanges (column -> row -> row -> column) through a padded shared tile whose
-//    faces lie N (mod 16) doubles apart and rows 17 apart, so the column and the row
-//    accesses of a half-warp hit 16 distinct 8-byte bank pairs;
-//  * the 1D matrices are kernel parameters (constant bank): every multiply-add is one DFMA
-//    and each line pass is N independent FMA chains;
-//  * results leave through coalesced stores.
+// (S (x) S) y^-1 (S^T (x) S^T) (preconditioner.py:96-110) as 1D line passes.
+//
+// Each WARP (N <= 16; a group of 4 warps for N = 17) works autonomously on batches of
+// FPW = 32 GW / N faces, with no CTA barriers:
+//  * thread 0 of the group streams the batches into a private ring of shared-memory stages
+//    with bulk async copies (cp.async.bulk + mbarrier transaction counts), S-1 batches
+//    ahead; a batch is contiguous in HBM, its 16-byte aligned cover is copied and the odd
+//    tail double (if any) is loaded before the arrive;
+//  * thread (f, l) owns line l of face f: a pass along the first index works on a COLUMN held
+//    in registers, a pass along the second index on a ROW; the four passes of Alg. 4 need
+//    two exchanges (column -> row -> row -> column) through a padded tile (faces N (mod 16)
+//    doubles apart, rows 17 apart: the column and row accesses of a half-warp hit 16
+//    distinct 8-byte bank pairs);
+//  * the 1D matrices are kernel parameters (constant bank): each line pass is N independent
+//    DFMA chains with uniform operands;
+//  * results leave through coalesced stores; the uniform-grid y^-1 class tables sit in
+//    shared memory.
 enum { FX_TRANSFORM = 0, FX_POST = 1, FX_PREC = 2, FX_INIT = 3, FX_UPDATE = 4 };
 
 template <int N, int FK>
 struct FxCfg {
   static constexpr int N2 = N * N;
-  static constexpr int FPB = (256 / N) & ~1;  // faces per batch (even: 16-byte batch offsets)
-  static constexpr int NT = 256;              // threads: one per (face, line), FPB * N <= 256 active
-  static constexpr int NP = 17;               // exchange row pitch, = 1 (mod 16)
+  static constexpr int GW = N > 16 ? 4 : 1;          // warps per face group (N = 17: 4 warps, 7 faces)
+  static constexpr int GT = 32 * GW;                 // threads per group
+  static constexpr int FPW = GT / N;                 // faces per group batch
+#ifndef HDGB_FX_WARPS
+#define HDGB_FX_WARPS 4
+#endif
+  static constexpr int WARPS = HDGB_FX_WARPS;        // warps per CTA
+  static constexpr int NG = WARPS / GW;              // independent groups per CTA
+  static constexpr int NT = 32 * WARPS;
+  static constexpr int NP = 17;                      // exchange row pitch, = 1 (mod 16)
   static constexpr int pad16(int x, int r) { return x + (((r - x) % 16) + 16) % 16; }
-  static constexpr int WP = pad16(N * NP, N % 16);  // exchange face pitch, = N (mod 16)
-  static constexpr int BAT = FPB * N2;              // doubles per staged batch
-  static constexpr int OPS = FK == FX_POST ? 2 : 1; // staged operands (G and u for the epilogue)
-  static constexpr int S = (FK == FX_POST || N >= 12) ? 2 : 3;  // ring stages
-  static constexpr int smem_doubles() { return S * OPS * BAT + FPB * WP; }
-  // register budget: CTAs per SM the shared memory allows anyway
-  static constexpr int MINB = (227 * 1024) / (8 * smem_doubles()) >= 4 ? 4 : ((227 * 1024) / (8 * smem_doubles()) >= 3 ? 3 : 2);
+  static constexpr int WP = pad16(N * NP, N % 16);   // exchange face pitch, = N (mod 16)
+  static constexpr int BATW = (FPW * N2 + 2 + 1) / 2 * 2;  // staged batch (+ alignment slack), even
+#ifdef HDGB_FX_S
+  static constexpr int S = HDGB_FX_S;
+#else
+  static constexpr int S = N <= 11 ? 3 : 2;          // ring stages per group
+#endif
+  static constexpr int EPT = (FPW * N2 + GT - 1) / GT;  // epilogue values per thread
+  static constexpr bool BLOCK = FK == FX_PREC || FK == FX_INIT || FK == FX_UPDATE;
+  // per-group slice, 128-byte aligned (bulk-copy destinations need 16)
+  __host__ __device__ static constexpr int per_group() { return (S * BATW + FPW * WP + 15) / 16 * 16; }
+  static constexpr int YT = BLOCK ? 9 * N2 : 0;      // uniform-grid y^-1 class tables
+  static constexpr int smem_doubles() { return NG * per_group() + (YT + 1) / 2 * 2; }
+#ifdef HDGB_FX_MINB
+  static constexpr int MINB = HDGB_FX_MINB;
+#else
+  // measured (config-3 sweep): capping registers for more resident CTAs raises DRAM traffic
+  // (L2 thrashing between the staged reads and the write-back) more than it hides latency
+  static constexpr int MINB = 2;
+#endif
 };
 
 // y[j] = sum_i M[j][i] x[i]: N independent chains, M from the constant bank
@@ -202,69 +226,83 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 template <int N, int FK, int CG>
-__global__ void __launch_bounds__(256, (FxCfg<N, FK>::MINB)) fx_kernel(const FaceArgs a, const uint8_t* __restrict__ finfo,
+__global__ void __launch_bounds__(FxCfg<N, FK>::NT, (FxCfg<N, FK>::MINB)) fx_kernel(const FaceArgs a, const uint8_t* __restrict__ finfo,
                                                                      const double* __restrict__ fcoef,
                                                                      const __grid_constant__ FxMats<N> M) {
   using C = FxCfg<N, FK>;
-  constexpr int N2 = C::N2, FPB = C::FPB, NT = C::NT, NP = C::NP, WP = C::WP, BAT = C::BAT, S = C::S;
-  constexpr int EPT = (FPB * N2 + NT - 1) / NT;  // epilogue values per thread
-  constexpr bool BLOCK = FK == FX_PREC || FK == FX_INIT || FK == FX_UPDATE;
+  constexpr int N2 = C::N2, FPW = C::FPW, NP = C::NP, WP = C::WP, BATW = C::BATW, S = C::S, GT = C::GT;
+  constexpr int GW = C::GW, EPT = C::EPT;
+  constexpr bool BLOCK = C::BLOCK;
   constexpr bool RED = FK == FX_INIT || FK == FX_UPDATE;
   constexpr bool POST = FK == FX_POST;
   constexpr bool ODD = N & 1;  // row-wise stores N doubles apart are bank-conflict-free
   if ((RED || (POST && CG)) && a.st->done) return;
   extern __shared__ __align__(128) double smem[];
-  double* sStage = smem;                      // S x [OPS x BAT]: staged batches (G, then u)
-  double* sW = smem + S * C::OPS * BAT;       // exchange tile, FPB x WP
-  __shared__ __align__(8) uint64_t sBar[S];
-  __shared__ uint8_t sInf[FPB];
-  __shared__ double sCoef[FPB];
+  __shared__ __align__(8) uint64_t sBar[C::NG][S];
   __shared__ double sWq[N];  // FX_POST: quadrature weights (dynamic index: keep out of the constant bank)
-  const int t = threadIdx.x, f = t / N, l = t - f * N;
-  if (POST && t < N) sWq[t] = M.B[t];
-  // FX_POST overwrites G (a.out) in place with r; a batch is staged before it is written
-  const double* src = POST ? a.out : a.in;
-  const int64_t nb = (a.nfaces + FPB - 1) / FPB;
-  const int64_t nmine = blockIdx.x < nb ? (nb - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  // producer: batch k of this CTA -> stage k % S
-  auto issue = [&](int64_t k) {
-    const int64_t bt = blockIdx.x + k * gridDim.x;
-    const int64_t f0 = bt * FPB;
-    const int nf = (int)min((int64_t)FPB, a.nfaces - f0);
-    const uint32_t vals = (uint32_t)nf * N2, bulk = vals & ~1u;  // odd tail: one plain double
-    double* dst = sStage + (k % S) * C::OPS * BAT;
-    uint64_t* bar = &sBar[k % S];
-    if (bulk != vals) {  // before the arrive, whose release makes it visible to the waiters
-      dst[bulk] = src[f0 * N2 + bulk];
-      if (POST) dst[BAT + bulk] = a.in[f0 * N2 + bulk];
-    }
-    mbar_expect_tx(bar, bulk * 8u * C::OPS);
-    bulk_g2s(dst, src + f0 * N2, bulk * 8u, bar);
-    if (POST) bulk_g2s(dst + BAT, a.in + f0 * N2, bulk * 8u, bar);
-  };
-  if (t == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&sBar[s], 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = warp / GW, gl = threadIdx.x - grp * GT;  // group and thread within it
+  const int f = gl / N, l = gl - (gl / N) * N;
+  const bool on_lane = f < FPW;
+  double* sStage = smem + grp * C::per_group();  // S x BATW
+  double* sW = sStage + S * BATW;                // FPW x WP exchange tile
+  double* sY = smem + C::NG * C::per_group();    // y^-1 class tables (uniform grids)
+  if (POST && threadIdx.x < N) sWq[threadIdx.x] = M.B[threadIdx.x];
+  if (BLOCK && a.ycls)
+    for (int t = threadIdx.x; t < C::YT; t += blockDim.x) sY[t] = a.ycls[t];
+  if (gl == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&sBar[grp][s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  __syncthreads();
-  if (t == 0)
+  __syncthreads();  // the only CTA-wide barrier: tables and barrier init
+  auto gsync = [&]() {
+    if (GW == 1) {
+      __syncwarp();
+    } else {
+      asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(GT) : "memory");
+    }
+  };
+  // FX_POST overwrites G (a.out) in place with r; each batch is staged before it is written
+  const double* src = POST ? a.out : a.in;
+  const int64_t nbat = (a.nfaces + FPW - 1) / FPW;
+  const int64_t gg = (int64_t)blockIdx.x * C::NG + grp, ngg = (int64_t)gridDim.x * C::NG;
+  const int64_t nmine = gg < nbat ? (nbat - 1 - gg) / ngg + 1 : 0;
+  // producer (thread 0 of the group): batch k -> stage k % S; the 16-byte aligned cover of
+  // the batch is bulk-copied, an odd tail double is loaded before the arrive (release)
+  auto issue = [&](int64_t k) {
+    const int64_t f0 = (gg + k * ngg) * FPW;
+    const int nf = (int)min((int64_t)FPW, a.nfaces - f0);
+    const int64_t s0 = f0 * N2, lo = s0 & ~(int64_t)1;
+    const uint32_t total = (uint32_t)(s0 - lo) + (uint32_t)nf * N2, bulk = total & ~1u;
+    double* dst = sStage + (k % S) * BATW;
+    uint64_t* bar = &sBar[grp][k % S];
+    if (bulk != total) dst[bulk] = src[lo + bulk];
+    mbar_expect_tx(bar, bulk * 8u);
+    bulk_g2s(dst, src + lo, bulk * 8u, bar);
+  };
+  if (gl == 0)
     for (int64_t k = 0; k < S - 1 && k < nmine; ++k) issue(k);
   double rz = 0.0;
   for (int64_t k = 0; k < nmine; ++k) {
-    if (t == 0 && k + S - 1 < nmine) {
-      fence_proxy_async();  // the stage's previous generic reads happen before the async refill
+    if (gl == 0 && k + S - 1 < nmine) {
+      fence_proxy_async();  // the stage's previous generic accesses happen before the refill
       issue(k + S - 1);
     }
-    const int64_t f0 = (blockIdx.x + k * gridDim.x) * FPB;
-    const int nf = (int)min((int64_t)FPB, a.nfaces - f0);
-    const bool on = f < nf;
-    if (t < nf) {
-      sInf[t] = finfo[f0 + t];
-      if (POST) sCoef[t] = fcoef[f0 + t];
+    const int64_t f0 = (gg + k * ngg) * FPW;
+    const int nf = (int)min((int64_t)FPW, a.nfaces - f0);
+    const int nv = nf * N2;
+    const bool on = on_lane && f < nf;
+    double* sX = sStage + (k % S) * BATW + (int)((f0 * N2) & 1);  // face fi at sX + fi * N2
+    const uint8_t inf = on ? finfo[f0 + f] : 0;
+    double uv[POST ? EPT : 1];
+    if (POST) {  // u for the epilogue, in flight during the passes (coalesced)
+#pragma unroll
+      for (int m = 0; m < EPT; ++m) {
+        const int it = gl + m * GT;
+        if (it < nv) uv[POST ? m : 0] = a.in[f0 * N2 + it];
+      }
     }
-    double* sO = sStage + (k % S) * C::OPS * BAT;  // the stage, reused for the result once read
-    const double* sX = sO;
-    mbar_wait(&sBar[k % S], (uint32_t)(k / S) & 1u);
+    mbar_wait(&sBar[grp][k % S], (uint32_t)(k / S) & 1u);
     double x[N], y[N], z[N];
     if (on) {  // pass 1 along the first index: column l
       const double* xs = sX + f * N2 + l;
@@ -275,21 +313,27 @@ __global__ void __launch_bounds__(256, (FxCfg<N, FK>::MINB)) fx_kernel(const Fac
 #pragma unroll
       for (int j = 0; j < N; ++j) ws[j * NP] = y[j];
     }
-    __syncthreads();
+    gsync();
     if (on) {  // pass 2 along the second index: row l
       double* wr = sW + f * WP + l * NP;
 #pragma unroll
       for (int c = 0; c < N; ++c) z[c] = wr[c];
       line_mv<N>(M.A, z, y);
       if (BLOCK) {  // * y^-1 (preconditioner.py:100-104), then pass 3 along the second index
-        const double* yi = a.ycls ? a.ycls + finfo_cls(sInf[f]) * N2 + l * N : a.yfull + (f0 + f) * N2 + l * N;
+        if (a.ycls) {
+          const double* yi = sY + finfo_cls(inf) * N2 + l * N;
 #pragma unroll
-        for (int kk = 0; kk < N; ++kk) y[kk] *= __ldg(yi + kk);
+          for (int kk = 0; kk < N; ++kk) y[kk] *= yi[kk];
+        } else {
+          const double* yi = a.yfull + (f0 + f) * N2 + l * N;
+#pragma unroll
+          for (int kk = 0; kk < N; ++kk) y[kk] *= __ldg(yi + kk);
+        }
         line_mv<N>(M.B, y, z);
 #pragma unroll
         for (int kk = 0; kk < N; ++kk) wr[kk] = z[kk];
       } else if (ODD) {  // result row straight into the consumed stage, contiguous
-        double* orow = sO + f * N2 + l * N;
+        double* orow = sX + f * N2 + l * N;
 #pragma unroll
         for (int kk = 0; kk < N; ++kk) orow[kk] = y[kk];
       } else {
@@ -298,13 +342,13 @@ __global__ void __launch_bounds__(256, (FxCfg<N, FK>::MINB)) fx_kernel(const Fac
       }
     }
     if (BLOCK) {
-      __syncthreads();
+      gsync();
       if (on) {  // pass 4 along the first index: column l; <r, z> from the same column
         double* wc = sW + f * WP + l;
 #pragma unroll
         for (int j = 0; j < N; ++j) z[j] = wc[j * NP];
         line_mv<N>(M.B, z, y);
-        const int kind = finfo_kind(sInf[f]);
+        const int kind = finfo_kind(inf);
         if (kind == HDGB_DIRICHLET) {  // zero_dirichlet (preconditioner.py:107)
 #pragma unroll
           for (int n = 0; n < N; ++n) y[n] = 0.0;
@@ -316,7 +360,7 @@ __global__ void __launch_bounds__(256, (FxCfg<N, FK>::MINB)) fx_kernel(const Fac
           rz += s;
         }
         if (ODD) {
-          double* ocol = sO + f * N2 + l;
+          double* ocol = sX + f * N2 + l;
 #pragma unroll
           for (int n = 0; n < N; ++n) ocol[n * N] = y[n];
         } else {
@@ -325,42 +369,39 @@ __global__ void __launch_bounds__(256, (FxCfg<N, FK>::MINB)) fx_kernel(const Fac
         }
       }
     }
-    __syncthreads();
-    // coalesced epilogue
+    gsync();
+    // coalesced epilogue over the batch
 #pragma unroll
     for (int m = 0; m < EPT; ++m) {
-      const int it = t + m * NT;
-      if (it >= nf * N2) break;
+      const int it = gl + m * GT;
+      if (it >= nv) break;
       const int fi = it / N2, q = it - fi * N2, j = q / N, kk = q - j * N;
       const int64_t gi = f0 * N2 + it;
-      // odd N: the result sits contiguous in the stage (conflict-free); even N: in the tile
-      double* wp = ODD ? sO + it : sW + fi * WP + j * NP + kk;
-      double v = *wp;
+      double v = ODD ? sX[it] : sW[fi * WP + j * NP + kk];
       if (POST) {
         // r = (sum_sides alpha_d GCC_ll) (w (x) w) u - (MS (x) MS) G
-        const double uv = sX[BAT + it];
-        v = ((sCoef[fi] * sWq[j]) * sWq[kk]) * uv - v;
+        const double u0 = uv[POST ? m : 0];
+        v = ((__ldg(fcoef + f0 + fi) * sWq[j]) * sWq[kk]) * u0 - v;
         if (CG) {
-          const int kind = finfo_kind(sInf[fi]);
+          const int kind = finfo_kind(__ldg(finfo + f0 + fi));
           if (kind == HDGB_DIRICHLET) v = 0.0;
-          sW[ODD ? it : fi * WP + j * NP + kk] = kind_counts(kind) ? uv * v : 0.0;
+          sX[it] = kind_counts(kind) ? u0 * v : 0.0;  // ODD: own slot; even: the stage is consumed
         }
       }
       a.out[gi] = v;
       if (FK == FX_INIT) a.p[gi] = v;
     }
-    if (POST && CG) {  // per-face <u, r>, fixed order
-      __syncthreads();
-      const int lane = t & 31, warp = t >> 5, nw = NT >> 5;
-      for (int fi = warp; fi < nf; fi += nw) {
+    if (POST && CG) {  // per-face <u, r>, fixed order; warp w of the group takes faces w, w+GW, ...
+      gsync();
+      for (int fi = warp - grp * GW; fi < nf; fi += GW) {
         double acc = 0.0;
-        for (int q = lane; q < N2; q += 32) acc += sW[ODD ? fi * N2 + q : fi * WP + (q / N) * NP + q % N];
+        for (int q = lane; q < N2; q += 32) acc += sX[fi * N2 + q];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) a.facedot[f0 + fi] = acc;
       }
     }
-    __syncthreads();
+    gsync();  // the stage and the tile are reused
   }
   if (RED) {
     double dummy = 0.0;
@@ -718,7 +759,7 @@ static cudaError_t fx_launch(hdgb_ctx* c, const FaceArgs& a, const double* Ah, c
   if (e != cudaSuccess) return e;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev);
-  const int64_t nb = (c->nfaces + C::FPB - 1) / C::FPB;
+  const int64_t nb = (c->nfaces + C::FPW * C::NG - 1) / (C::FPW * C::NG);
   int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
   if (grid > PW_GRID) grid = PW_GRID;
   if (grid > nb) grid = nb;
