@@ -120,6 +120,13 @@ int64_t hdgb_dot_scratch_doubles(void);
 /* *result_dev = sum_i x_i y_i (deterministic fixed-order reduction). */
 int hdgb_vec_dot(const double* x, const double* y, int64_t n, double* scratch_dev, double* result_dev,
                  void* stream);
+/* *result_dev = sum of x_i y_i over the all-face vectors' positions on faces that count:
+ * Dirichlet faces and the peer copy of a slab interface plane (HDGB_HALO_PEER) are skipped,
+ * so the sum over ranks of the rank-local values is the global dot of the unknowns
+ * (the per-rank term of the distributed pcg's allreduce).  Same scratch as
+ * hdgb_vec_dot; deterministic fixed-order reduction. */
+int hdgb_face_dot(hdgb_ctx* ctx, const double* x, const double* y, double* scratch_dev, double* result_dev,
+                  void* stream);
 /* out = a*x + b*y (out may alias x or y). */
 int hdgb_vec_axpby(int64_t n, double a, const double* x, double b, const double* y, double* out, void* stream);
 

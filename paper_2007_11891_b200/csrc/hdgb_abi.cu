@@ -13,6 +13,8 @@ cudaError_t launch_cg_init(hdgb_ctx* c, int kind, cudaStream_t s);
 cudaError_t launch_reduce_pw(hdgb_ctx* c, cudaStream_t s);
 cudaError_t launch_p_update(hdgb_ctx* c, cudaStream_t s, cudaGraphConditionalHandle loop, int has_loop);
 cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* scratch, double* result, cudaStream_t s);
+cudaError_t launch_face_dot(hdgb_ctx* c, const double* x, const double* y, double* scratch, double* result,
+                            cudaStream_t s);
 cudaError_t launch_axpby(int64_t n, double a, const double* x, double b, const double* y, double* out, cudaStream_t s);
 cudaError_t launch_pack(hdgb_ctx* c, int mode, const double* in, double* out, cudaStream_t s);
 cudaError_t launch_halo(hdgb_ctx* c, int mode, int plane, double* all, double* buf, cudaStream_t s);
@@ -387,6 +389,16 @@ int hdgb_vec_dot(const double* x, const double* y, int64_t n, double* scratch, d
     return HDGB_OK;
   }
   HDGB_CUDA(launch_dot(x, y, n, scratch, result, (cudaStream_t)stream));
+  return HDGB_OK;
+}
+
+int hdgb_face_dot(hdgb_ctx* c, const double* x, const double* y, double* scratch, double* result, void* stream) {
+  if (!c || !x || !y || !scratch || !result) return einval("null argument");
+  if (c->n_all == 0) {
+    HDGB_CUDA(cudaMemsetAsync(result, 0, sizeof(double), (cudaStream_t)stream));
+    return HDGB_OK;
+  }
+  HDGB_CUDA(launch_face_dot(c, x, y, scratch, result, (cudaStream_t)stream));
   return HDGB_OK;
 }
 

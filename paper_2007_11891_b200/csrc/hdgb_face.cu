@@ -467,6 +467,24 @@ __global__ void __launch_bounds__(HDGB_NT) dot_kernel(const double* __restrict__
   }
 }
 
+// <x, y> over the faces that count (not Dirichlet, not the peer copy of a slab interface):
+// the rank-local part of a distributed dot; fixed grid, fixed order
+__global__ void __launch_bounds__(HDGB_NT) face_dot_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                                           const uint8_t* __restrict__ finfo, unsigned N2, int64_t n,
+                                                           double* part, uint32_t* cnt, double* result) {
+  double s = 0.0, dummy = 0.0;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * per, b1 = min(n, b0 + per);
+  for (int64_t q = b0 + threadIdx.x; q < b1; q += blockDim.x)
+    if (kind_counts(finfo_kind(__ldg(finfo + (unsigned)q / N2)))) s = fma(x[q], y[q], s);
+  block_sum2(s, dummy);
+  if (publish_last(part, s, 0.0, cnt)) {
+    double t, z;
+    final_sum2(part, gridDim.x, t, z);
+    if (threadIdx.x == 0) *result = t;
+  }
+}
+
 __global__ void axpby_kernel(int64_t n, double a, const double* x, double b, const double* y, double* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = a * x[i] + b * y[i];
@@ -921,6 +939,16 @@ cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* scra
   int grid = (int)min((int64_t)HDGB_RED_BLOCKS, max((int64_t)1, (n + 2047) / 2048));
   uint32_t* cnt = reinterpret_cast<uint32_t*>(scratch + 2 * HDGB_RED_BLOCKS);
   dot_kernel<<<grid, HDGB_NT, 0, s>>>(x, y, n, scratch, cnt, result);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_face_dot(hdgb_ctx* c, const double* x, const double* y, double* scratch, double* result,
+                            cudaStream_t s) {
+  const int64_t n = c->n_all;
+  int grid = (int)min((int64_t)HDGB_RED_BLOCKS, max((int64_t)1, (n + 2047) / 2048));
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(scratch + 2 * HDGB_RED_BLOCKS);
+  face_dot_kernel<<<grid, HDGB_NT, 0, s>>>(x, y, c->d_finfo, (unsigned)(c->N * c->N), n, scratch, cnt, result);
+  c->launches++;
   return cudaGetLastError();
 }
 

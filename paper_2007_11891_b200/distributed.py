@@ -15,11 +15,13 @@ The transport is torch.distributed (NCCL on GPUs, gloo in the CPU tests); the
 plane gather/scatter runs in the library's halo kernels on the device.
 """
 
+import math
+
 import numpy as np
 
 from . import _lib
 
-__all__ = ["slab_range", "slab_side_kinds", "slab_mesh", "SlabHalo"]
+__all__ = ["slab_range", "slab_side_kinds", "slab_mesh", "SlabHalo", "slab_pcg", "SlabSystem"]
 
 
 def slab_range(n1, rank, world):
@@ -115,3 +117,96 @@ def owned_mask_x(n_faces0, n1, rank, world):
     f = np.arange(n_faces0)
     plane = f % (n1 + 1)
     return ~((plane == 0) & (rank > 0))
+
+
+def _allreduce_sum(vals, group=None):
+    """Sum a list of rank-local scalar tensors over the ranks (one collective); floats out."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.stack([v.reshape(()) for v in vals])
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(t, group=group)
+    return [float(v) for v in t.tolist()]
+
+
+def slab_pcg(apply_K, apply_P, F, x0, dot, axpby, rtol=1e-10, atol=0.0, max_iters=10000, allreduce=None):
+    """PCG of solver.py:282-321 on an x-slab partition.
+
+    Rank-local vectors in the all-face layout (Dirichlet slots zero); `apply_K` includes the
+    interface exchange, `dot(a, b)` is the rank-local owned-face dot (a scalar tensor) and
+    `allreduce` sums a list of them over the ranks.  Two reductions per iteration: <p, w>,
+    then (||r||^2, <r, z>) fused - z = P r is formed before the convergence test, which only
+    adds one preconditioner apply on the final iteration.  Same stopping rule, early exits
+    and FloatingPointError conditions as the reference.
+    """
+    allreduce = allreduce or _allreduce_sum
+    x = x0.clone()
+    r = axpby(1.0, F, -1.0, apply_K(x))
+    z = apply_P(r) if apply_P is not None else r
+    rr, rz = allreduce([dot(r, r), dot(r, z)])
+    norm0 = math.sqrt(rr) if rr >= 0.0 else float("nan")
+    if not math.isfinite(norm0):
+        raise FloatingPointError("non-finite initial residual")
+    if norm0 == 0.0 or norm0 <= atol:
+        return x, 0, 0.0, True
+    threshold = max(rtol * norm0, atol)
+    rho = rz
+    p = z.clone()
+    rn = norm0
+    for it in range(1, max_iters + 1):
+        w = apply_K(p)
+        (curv,) = allreduce([dot(p, w)])
+        if not math.isfinite(curv) or curv <= 0.0:
+            raise FloatingPointError("conjugate gradient breakdown: non-positive curvature")
+        alpha = rho / curv
+        x = axpby(1.0, x, alpha, p, out=x)
+        r = axpby(1.0, r, -alpha, w, out=r)
+        z = apply_P(r) if apply_P is not None else r
+        rr, rz = allreduce([dot(r, r), dot(r, z)])
+        rn = math.sqrt(rr) if rr >= 0.0 else float("nan")
+        if not math.isfinite(rn):
+            raise FloatingPointError("non-finite residual during iteration")
+        if rn <= threshold:
+            return x, it, rn / norm0, True
+        beta = rz / rho
+        rho = rz
+        p = axpby(1.0, z, beta, p)
+    return x, max_iters, rn / norm0, False
+
+
+class SlabSystem:
+    """Device operator, preconditioner and owned-face dots of one slab rank.
+
+    K v = (local apply, Dirichlet rows zeroed) + interface exchange; P = face-local
+    preconditioner (`prec` kind, or None); dots through `hdgb_face_dot`.
+    """
+
+    def __init__(self, dc, halo=None, variant=0, prec=_lib.PREC_BLOCK, group=None):
+        import torch
+
+        self.dc, self.halo, self.variant, self.prec, self.group = dc, halo, variant, prec, group
+        self._red = torch.zeros(2, dtype=torch.float64, device=f"cuda:{dc.device}")
+        from .solver import _Vec
+
+        self._vec = _Vec(torch.device("cuda", dc.device))
+
+    def K(self, v):
+        w = self.dc.apply(v, self.variant)
+        self.dc.zero_dirichlet(w)
+        if self.halo is not None:
+            self.halo.exchange_add(w)
+        return w
+
+    def P(self, r):
+        return self.dc.prec(r, self.prec)
+
+    def dot(self, a, b):
+        import torch
+
+        out = torch.empty(1, dtype=torch.float64, device=a.device)
+        return self.dc.face_dot(a, b, out)
+
+    def solve(self, F, x0, rtol=1e-10, atol=0.0, max_iters=10000):
+        return slab_pcg(self.K, self.P if self.prec is not None else None, F, x0, self.dot, self._vec.axpby, rtol,
+                        atol, max_iters, allreduce=lambda vals: _allreduce_sum(vals, self.group))

@@ -256,6 +256,19 @@ class DeviceContext:
                                           self.stream()))
         return out
 
+    def face_dot(self, x, y, out):
+        """out[0] = <x, y> over the faces that count (not Dirichlet, not a slab-interface peer copy)."""
+        import torch
+
+        sc = getattr(self, "_dot_scratch", None)
+        if sc is None:
+            sc = self._dot_scratch = torch.zeros(int(_lib.lib().hdgb_dot_scratch_doubles()), dtype=torch.float64,
+                                                 device=f"cuda:{self.device}")
+        _lib.check(_lib.lib().hdgb_face_dot(self.handle, self.check_vec(x), self.check_vec(y),
+                                            ctypes.c_void_p(sc.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                            self.stream()))
+        return out
+
     def zero_dirichlet(self, allv):
         _lib.check(_lib.lib().hdgb_zero_dirichlet(self.handle, self.check_vec(allv), self.stream()))
         return allv

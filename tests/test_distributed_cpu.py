@@ -16,7 +16,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import hdg_oracle as O
-from paper_2007_11891_b200.distributed import SlabHalo, owned_mask_x, slab_range, slab_side_kinds
+from paper_2007_11891_b200.distributed import SlabHalo, owned_mask_x, slab_pcg, slab_range, slab_side_kinds
 from paper_2007_11891_b200 import _lib
 
 
@@ -110,6 +110,98 @@ def test_slab_halo_exchange_matches_global_operator(p):
     for rank, err, dsum, dglob in res:
         assert err < 1e-13, (rank, err)
         assert abs(dsum - dglob) <= 1e-12 * abs(dglob)
+
+
+def _pcg_worker(rank, world, port, m, p, q):
+    """Distributed block-PCG (slab_pcg) on gloo vs the global oracle PCG."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = p + 1
+        N2 = n * n
+        gn = (m * world, m, m)
+        gctx = O.problem(gn, p, 0.7, hi=(float(world), 1.0, 1.0))
+        grid = gctx["grid"]
+        y = O.face_selfcoupling(gctx)
+        Fp = np.random.default_rng(9).uniform(-1, 1, grid.n_unknowns(n))
+        xo, ito, relo, _ = O.pcg(lambda v: O.apply_op_packed(gctx, v),
+                                 lambda r: O.pack(grid, n, O.block_prec_apply(gctx, y, O.unpack(grid, n, r))),
+                                 Fp, np.zeros_like(Fp), rtol=1e-10)
+        x_glob = O.unpack(grid, n, xo)
+        F_glob = O.unpack(grid, n, Fp)
+        i0, i1 = slab_range(gn[0], rank, world)
+        ln = (i1 - i0, m, m)
+        # interface sides are unknown (not Dirichlet) on the local grid
+        bc = ["dirichlet"] * 6
+        if rank > 0:
+            bc[0] = "neumann"
+        if rank < world - 1:
+            bc[1] = "neumann"
+        lctx = O.context(gctx["basis"], O.Grid.uniform(ln, (float(i0) / m, 0, 0), (float(i1) / m, 1, 1), tuple(bc)),
+                         0.7)
+        lgrid = lctx["grid"]
+        idx = _local_to_global(gn, ln, i0, n)
+        Y = np.concatenate([yd.ravel() for yd in y])[idx]
+        offs = lgrid.offsets(n)
+        y_loc = [Y[offs[d]:offs[d + 1]].reshape(lgrid.n_faces[d], n, n) for d in range(3)]
+        unk = torch.from_numpy(lgrid.unknown_mask(n))
+        l1 = ln[0]
+        own_x = owned_mask_x((l1 + 1) * m * m, l1, rank, world)
+        own = torch.from_numpy(np.concatenate([np.repeat(own_x, N2), np.ones(len(idx) - own_x.size * N2, bool)])) & unk
+
+        def pack(vec, plane):
+            f = plane + (l1 + 1) * np.arange(m * m)
+            return vec[torch.from_numpy((f[:, None] * N2 + np.arange(N2)[None, :]).ravel())].clone()
+
+        def add(vec, plane, buf):
+            f = plane + (l1 + 1) * np.arange(m * m)
+            vec[torch.from_numpy((f[:, None] * N2 + np.arange(N2)[None, :]).ravel())] += buf
+
+        halo = SlabHalo(None, rank, world, pack=pack, add=add, n1=l1, plane_len=m * m * N2,
+                        empty=lambda: torch.empty(m * m * N2, dtype=torch.float64))
+
+        def K(v):
+            w = torch.from_numpy(O.apply_op(lctx, v.numpy()))
+            w[~unk] = 0.0
+            return halo.exchange_add(w)
+
+        def P(r):
+            return torch.from_numpy(O.block_prec_apply(lctx, y_loc, r.numpy()))
+
+        def axpby(a, x, b, yv, out=None):
+            res = a * x + b * yv
+            if out is None:
+                return res
+            out.copy_(res)
+            return out
+
+        x, it, rel, conv = slab_pcg(K, P, torch.from_numpy(F_glob[idx]), torch.zeros(len(idx), dtype=torch.float64),
+                                    lambda a, b: (a * b)[own].sum(), axpby, rtol=1e-10)
+        err = float(np.max(np.abs(x.numpy() - x_glob[idx])) / np.max(np.abs(x_glob)))
+        q.put((rank, it, ito, conv, err, rel, relo))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_slab_pcg_matches_global_pcg(p):
+    world, m = 2, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pcg_worker, args=(r, world, port, m, p, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    its = {r[1] for r in res}
+    assert len(its) == 1  # every rank sees the same reductions
+    for rank, it, ito, conv, err, rel, relo in res:
+        assert conv and abs(it - ito) <= 1, (it, ito)
+        assert err < 1e-9, (rank, err)
 
 
 def test_slab_ranges_cover_the_grid():

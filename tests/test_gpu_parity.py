@@ -303,3 +303,31 @@ def test_odd_length_vectors_and_alignment():
     buf = torch.zeros(mesh.n_all(p) + 1, dtype=torch.float64, device="cuda")
     with pytest.raises(ValueError, match="aligned"):
         dc.apply(buf[1:], 0)
+
+
+@pytest.mark.parametrize("name,kind", [("block", 1), ("none", None)])
+def test_slab_system_single_rank_matches_reference(name, kind):
+    """Distributed PCG driver (owned-face dots, two reductions per iteration) on one rank."""
+    from paper_2007_11891_b200.distributed import SlabSystem
+
+    g = load("cfg1")
+    mesh, ctx = _mesh_ctx(g)
+    dc = hb.device_context(ctx)
+    Fd = dc.unpack(_dev(g["sin_F"]))
+    x, it, rel, conv = SlabSystem(dc, prec=kind).solve(Fd, torch.zeros_like(Fd), rtol=1e-10)
+    ref_it = int(g[f"sin_{name}_it"])
+    tol_it = 1 if name != "none" else max(1, int(0.02 * ref_it))
+    assert conv and abs(it - ref_it) <= tol_it, (it, ref_it)
+    assert relerr(dc.pack(x).cpu().numpy(), g[f"sin_{name}_x"]) < 1e-8
+
+
+def test_face_dot_counts_unknown_faces_once():
+    g = load("mixed")
+    mesh, ctx = _mesh_ctx(g)
+    dc = hb.device_context(ctx)
+    rng = np.random.default_rng(4)
+    a, b = rng.standard_normal(mesh.n_all(ctx.basis.p)), rng.standard_normal(mesh.n_all(ctx.basis.p))
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    dc.face_dot(_dev(a), _dev(b), out)
+    pa, pb = hb.pack_unknowns(hb.unpack_all(a, mesh, ctx.basis.p)), hb.pack_unknowns(hb.unpack_all(b, mesh, ctx.basis.p))
+    assert abs(float(out.item()) - float(np.dot(pa, pb))) <= 1e-12 * np.abs(pa * pb).sum()
