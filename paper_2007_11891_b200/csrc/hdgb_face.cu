@@ -121,8 +121,8 @@ __global__ void __launch_bounds__(256) pw_kernel(FaceArgs a, const uint8_t* __re
 // tensor-product operators (A (x) A) X = A X A^T and the block preconditioner
 // (S (x) S) y^-1 (S^T (x) S^T) (preconditioner.py:96-110) as 1D line passes.
 //
-// Each WARP (N <= 16; a group of 4 warps for N = 17) works autonomously on batches of
-// FPW = 32 GW / N faces, with no CTA barriers:
+// Each group of GW warps (GW = 1, 2 or 4, chosen per N for lane utilization)
+// works autonomously on batches of FPW = 32 GW / N faces, with no CTA barriers:
 //  * thread 0 of the group streams the batches into a private ring of shared-memory stages
 //    with bulk async copies (cp.async.bulk + mbarrier transaction counts), S-1 batches
 //    ahead; a batch is contiguous in HBM, its 16-byte aligned cover is copied and the odd
@@ -141,7 +141,10 @@ enum { FX_TRANSFORM = 0, FX_POST = 1, FX_PREC = 2, FX_INIT = 3, FX_UPDATE = 4 };
 template <int N, int FK>
 struct FxCfg {
   static constexpr int N2 = N * N;
-  static constexpr int GW = N > 16 ? 4 : 1;          // warps per face group (N = 17: 4 warps, 7 faces)
+  // warps per face group: the smallest of 1, 2, 4 keeping >= 80 % of the lanes on a line,
+  // except N = 9, where 2 warps (7 faces, 98 %) measured faster than 1 (3 faces, 84 %)
+  static constexpr int util(int gw) { return 100 * N * ((32 * gw) / N) / (32 * gw); }
+  static constexpr int GW = N == 9 ? 2 : (util(1) >= 80 ? 1 : (util(2) >= 80 ? 2 : 4));
   static constexpr int GT = 32 * GW;                 // threads per group
   static constexpr int FPW = GT / N;                 // faces per group batch
 #ifndef HDGB_FX_WARPS
