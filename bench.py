@@ -419,6 +419,30 @@ def run_ours(args):
               "hbm_frac_of_96B_per_unknown": (96 * N_all / (t_cg / it) / 1e9) / hbm,
               "note": "whole solve incl. setup kernels, one CUDA graph with device-side while loop; "
                       "config-2 vectors are L2-resident during the solve"}
+        # transformed pipeline (solve_transformed, solver.py:372-410): F_hat = (S^T (x) S^T) F,
+        # Alg. 3 operator + eigen-diagonal preconditioner (= the block preconditioner in that basis)
+        Fh = dc.transform(Fd, np.ascontiguousarray(ctx.basis.S.T))
+        dc.zero_dirichlet(Fh)
+        for _ in range(2):
+            x.zero_()
+            dc.pcg(1, 3, Fh, x, 1e-10, 0.0, 10000)
+        tr_ms = []
+        for _ in range(5):
+            flush.zero_()
+            x.zero_()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            it_t, rel_t, conv_t = dc.pcg(1, 3, Fh, x, 1e-10, 0.0, 10000)
+            b.record(stream)
+            b.synchronize()
+            tr_ms.append(a.elapsed_time(b))
+        t_tr_cg = statistics.median(tr_ms) * 1e-3
+        cg["transformed"] = {"preconditioner": "eigen diagonal (transformed_preconditioner)", "iterations": it_t,
+                             "converged": conv_t, "relres": rel_t, "solve_ms": t_tr_cg * 1e3,
+                             "ms_per_iter": t_tr_cg / it_t * 1e3,
+                             "us_per_unknown_per_iter": t_tr_cg / it_t / N * 1e6}
 
     if world > 1:
         try:

@@ -773,15 +773,11 @@ static cudaError_t fx_launch(hdgb_ctx* c, const FaceArgs& a, const double* Ah, c
   }
   const size_t smem = sizeof(double) * C::smem_doubles();
   auto k = fx_kernel<N, FK, CG>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static int cache[16] = {0};
+  int64_t grid = 0;
+  cudaError_t e = resident_grid(k, C::NT, smem, c->dev, cache, &grid);
   if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, C::NT, smem);
-  if (e != cudaSuccess) return e;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev);
   const int64_t nb = (c->nfaces + C::FPW * C::NG - 1) / (C::FPW * C::NG);
-  int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
   if (grid > PW_GRID) grid = PW_GRID;
   if (grid > nb) grid = nb;
   if (grid < 1) grid = 1;

@@ -293,6 +293,28 @@ cudaError_t launch_build_tables(hdgb_ctx* c, cudaStream_t s);
 cudaError_t op_set_smem_limits(hdgb_ctx* c);
 }  // namespace hdgb
 
+namespace hdgb {
+// Resident CTAs x SMs of a kernel with `smem` dynamic shared memory on device `dev`, with its
+// shared-memory limit raised once per device.  `Cache` is a per-kernel static (the host
+// launch path is otherwise dominated by attribute queries at small problem sizes).
+template <typename Kern>
+inline cudaError_t resident_grid(Kern kern, int threads, size_t smem, int dev, int* cache, int64_t* grid) {
+  if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
+  if (cache[dev] <= 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    cache[dev] = (per_sm > 0 ? per_sm : 1) * sms;
+  }
+  *grid = cache[dev];
+  return cudaSuccess;
+}
+}  // namespace hdgb
+
 #define HDGB_CUDA(call)                                 \
   do {                                                  \
     cudaError_t _e = (call);                            \

@@ -307,15 +307,11 @@ static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
   using Cf = OpVCfg<N>;
   const size_t smem = sizeof(double) * (size_t)Cf::smem_doubles(MODE & 1);
   auto kern = opV_kernel<N, MODE, COLOR>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static int cache[16] = {0};
+  int64_t grid = 0;
+  cudaError_t e = resident_grid(kern, Cf::NT, smem, c->dev, cache, &grid);
   if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cf::NT, smem);
-  if (e != cudaSuccess) return e;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev);
   const int64_t need = (t1 - t0 + Cf::G - 1) / Cf::G;
-  int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
   if (grid > need) grid = need;
   if (grid < 1) return cudaSuccess;
   TabOff to;
