@@ -115,6 +115,19 @@ int hdgb_zero_dirichlet(hdgb_ctx* ctx, double* all, void* stream);
 int hdgb_pcg(hdgb_ctx* ctx, int variant, int prec, const double* F, double* x, double rtol, double atol,
              int32_t max_iters, int32_t* iters, double* relres, int32_t* converged, void* stream);
 
+/* ---- element-local pre/post of the condensed solve ----
+ * Reference-element tables of the interior solver: D = M Dhat (n*n, row-major), B and C
+ * (n*2, row-major), host pointers (basis.py:96-120).  Required by the two calls below. */
+int hdgb_ctx_set_element_tables(hdgb_ctx* ctx, const double* D, const double* B, const double* C);
+/* F (all faces) = element part of build_rhs (solver.py:212-251): -sum over elements of the flux
+ * couplings of A^-1 (M3 f, 0), Dirichlet faces included (the caller adds Neumann data, subtracts
+ * the Dirichlet lift K g_D and zeroes Dirichlet rows).  f: n_e * n^3 element values
+ * (element-major, a1 slowest). */
+int hdgb_build_rhs(hdgb_ctx* ctx, const double* f, double* F, void* stream);
+/* recover_interior (solver.py:254-279): u (n_e * n^3) and q (3 * n_e * n^3, direction-major)
+ * from f and the all-face trace. */
+int hdgb_recover_interior(hdgb_ctx* ctx, const double* f, const double* trace, double* u, double* q, void* stream);
+
 /* Generic FP64 vector kernels for pcg() with arbitrary callables (solver.py:282-321). */
 int64_t hdgb_dot_scratch_doubles(void);
 /* *result_dev = sum_i x_i y_i (deterministic fixed-order reduction). */

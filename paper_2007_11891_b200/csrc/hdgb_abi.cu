@@ -392,6 +392,31 @@ int hdgb_vec_dot(const double* x, const double* y, int64_t n, double* scratch, d
   return HDGB_OK;
 }
 
+int hdgb_ctx_set_element_tables(hdgb_ctx* c, const double* D, const double* B, const double* C) {
+  if (!c || !D || !B || !C) return einval("null argument");
+  const int N = c->N;
+  c->h_elem.assign(D, D + N * N);
+  c->h_elem.insert(c->h_elem.end(), B, B + 2 * N);
+  c->h_elem.insert(c->h_elem.end(), C, C + 2 * N);
+  return HDGB_OK;
+}
+
+int hdgb_build_rhs(hdgb_ctx* c, const double* f, double* F, void* stream) {
+  if (!c || !f || !F) return einval("null argument");
+  if (c->h_elem.empty()) return einval("element tables not set (hdgb_ctx_set_element_tables)");
+  if (c->g.ne == 0) return HDGB_OK;
+  HDGB_CUDA(launch_build_rhs(c, f, F, (cudaStream_t)stream));
+  return HDGB_OK;
+}
+
+int hdgb_recover_interior(hdgb_ctx* c, const double* f, const double* trace, double* u, double* q, void* stream) {
+  if (!c || !f || !trace || !u || !q) return einval("null argument");
+  if (c->h_elem.empty()) return einval("element tables not set (hdgb_ctx_set_element_tables)");
+  if (c->g.ne == 0) return HDGB_OK;
+  HDGB_CUDA(launch_recover(c, f, trace, u, q, (cudaStream_t)stream));
+  return HDGB_OK;
+}
+
 int hdgb_face_dot(hdgb_ctx* c, const double* x, const double* y, double* scratch, double* result, void* stream) {
   if (!c || !x || !y || !scratch || !result) return einval("null argument");
   if (c->n_all == 0) {

@@ -187,6 +187,9 @@ class DeviceContext:
         with torch.cuda.device(self.device):
             _lib.check(L.hdgb_ctx_create(ctypes.byref(desc), ctypes.byref(handle)))
         self.handle = handle
+        # reference-element tables of the interior solver (device build_rhs / recover_interior)
+        Dm, Bm, Cm = (np.ascontiguousarray(getattr(basis, k), dtype=np.float64) for k in ("D", "B", "C"))
+        _lib.check(L.hdgb_ctx_set_element_tables(handle, _lib.dptr(Dm), _lib.dptr(Bm), _lib.dptr(Cm)))
         self.n_all = int(L.hdgb_ctx_n_all(handle))
         self.n_unknown = int(L.hdgb_ctx_n_unknown(handle))
         self._scratch = None
@@ -255,6 +258,35 @@ class DeviceContext:
         _lib.check(_lib.lib().hdgb_unpack(self.handle, self.check_vec(packed, self.n_unknown), self.check_vec(out),
                                           self.stream()))
         return out
+
+    def build_rhs(self, f):
+        """Element part of build_rhs (solver.py:212-251) on the device: all-face F, Dirichlet rows
+        included (the caller adds Neumann data, the Dirichlet lift and zeroes Dirichlet rows)."""
+        import torch
+
+        f = torch.as_tensor(f, dtype=torch.float64).to(f"cuda:{self.device}").contiguous()
+        if f.numel() != self.mesh.n_elements * self.n ** 3:
+            raise ValueError("f must hold n_elements * (p+1)^3 values")
+        F = self.empty()
+        _lib.check(_lib.lib().hdgb_build_rhs(self.handle, ctypes.c_void_p(f.data_ptr()), self.check_vec(F),
+                                             self.stream()))
+        return F
+
+    def recover_interior(self, f, trace):
+        """(u, (q1, q2, q3)) from f and the all-face trace (solver.py:254-279), device tensors."""
+        import torch
+
+        ne, n3 = self.mesh.n_elements, self.n ** 3
+        f = torch.as_tensor(f, dtype=torch.float64).to(f"cuda:{self.device}").contiguous()
+        if f.numel() != ne * n3:
+            raise ValueError("f must hold n_elements * (p+1)^3 values")
+        u = torch.empty(ne * n3, dtype=torch.float64, device=f"cuda:{self.device}")
+        q = torch.empty(3 * ne * n3, dtype=torch.float64, device=f"cuda:{self.device}")
+        _lib.check(_lib.lib().hdgb_recover_interior(self.handle, ctypes.c_void_p(f.data_ptr()), self.check_vec(trace),
+                                                    ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(q.data_ptr()),
+                                                    self.stream()))
+        shape = (ne,) + (self.n,) * 3
+        return u.view(shape), tuple(q[d * ne * n3:(d + 1) * ne * n3].view(shape) for d in range(3))
 
     def face_dot(self, x, y, out):
         """out[0] = <x, y> over the faces that count (not Dirichlet, not a slab-interface peer copy)."""

@@ -10,10 +10,13 @@ the library's deterministic FP64 dot/axpby kernels.
 
 Pre/post steps (element inverse by fast diagonalisation, RHS with
 Dirichlet lift, hybridised initial guess, interior recovery;
-solver.py:129-279) run once per solve and are outside the hot path
-(SURVEY §2 / §8f "next" #1): they stay host-side numpy here, generalised to
-per-element geometry for non-uniform grids, and use the device operator
-for the Dirichlet lift.
+solver.py:129-279; SURVEY §8f "next" #1): `solve` / `solve_transformed`
+run the element RHS and the interior recovery on the device
+(csrc/hdgb_elem.cu) and keep every vector device-resident from the RHS to
+(u, q); the host restatements below (generalised to per-element geometry
+for non-uniform grids) remain the public pre/post functions, the parity
+reference of the device versions, and the path taken when a FlopCounter
+is attached (it counts per host call).
 """
 
 import math
@@ -24,7 +27,8 @@ import numpy as np
 
 from . import _lib
 from .basis import Basis1D
-from .mesh import DIRICHLET, NEUMANN, FluxField, gather_batched, pack_unknowns, scatter_add_batched, unpack_unknowns
+from .mesh import (DIRICHLET, NEUMANN, FluxField, gather_batched, pack_all, pack_unknowns, scatter_add_batched,
+                   unpack_unknowns)
 from .operator import OperatorContext, device_context, hdg_op_3d, transform_faces
 from .preconditioner import (
     BlockPreconditioner,
@@ -487,10 +491,73 @@ def _ops(ctx):
     return c.ops if c is not None else None
 
 
+_PREC_KIND = {"none": _lib.PREC_NONE, "diagonal": _lib.PREC_DIAG_NODAL, "block": _lib.PREC_BLOCK}
+
+
+def _solve_device(u0, f, g_D, g_N, cfg, ctx, transformed):
+    """Device-resident solve: element RHS, fused PCG and interior recovery on the GPU.
+
+    Host work is limited to the boundary data (Neumann face masses, the Dirichlet lift
+    vector) and a non-zero initial guess (hybridize_initial_guess).
+    """
+    import torch
+
+    dc = device_context(ctx)
+    mesh, p = ctx.mesh, ctx.basis.p
+    dev = f"cuda:{dc.device}"
+    F = dc.build_rhs(f)
+    if g_N is not None:  # Neumann data (solver.py:233-237)
+        neu = FluxField(mesh, p)
+        for d in range(3):
+            m = mesh.face_kind[d] == NEUMANN
+            if np.any(m):
+                fm = _face_mass(ctx, d)
+                neu.data[d][m] = (fm[0] if fm.shape[0] == 1 else fm[m]) * g_N.data[d][m]
+        F += torch.from_numpy(pack_all(neu)).to(dev)
+    lift = None
+    if g_D is not None:  # Dirichlet lift (solver.py:239-249)
+        lf = FluxField(mesh, p)
+        for d in range(3):
+            m = mesh.face_kind[d] == DIRICHLET
+            lf.data[d][m] = g_D.data[d][m]
+        if any(np.any(x) for x in lf.data):
+            lift = torch.from_numpy(pack_all(lf)).to(dev)
+            F -= dc.apply(lift, _lib.PLAIN)
+    dc.zero_dirichlet(F)
+    u0a = np.asarray(u0, dtype=float)
+    if np.any(u0a) or g_D is not None or g_N is not None:
+        x = torch.from_numpy(pack_all(hybridize_initial_guess(u0a, ctx, g_D, g_N))).to(dev)
+    else:
+        x = torch.zeros(dc.n_all, dtype=torch.float64, device=dev)
+    if transformed:  # Alg. 6: solve in the eigenbasis (solver.py:381-399)
+        F = dc.zero_dirichlet(dc.transform(F, np.ascontiguousarray(ctx.basis.S.T)))
+        x = dc.transform(x, np.ascontiguousarray(ctx.T))
+        variant, kind = _lib.TRANSFORMED, _lib.PREC_DIAG_EIGEN
+    else:
+        variant, kind = _lib.PLAIN, _PREC_KIND[cfg.preconditioner]
+    torch.cuda.synchronize(dc.device)
+    t0 = time.perf_counter()
+    iters, relres, conv = dc.pcg(variant, kind, F, x, cfg.rtol, cfg.atol, cfg.max_iters)
+    wall = time.perf_counter() - t0
+    if transformed:
+        x = dc.transform(x, np.ascontiguousarray(ctx.basis.S))
+    if lift is not None:
+        x += lift  # _restore_dirichlet: Dirichlet slots are zero after the solve
+    u, qs = dc.recover_interior(f, x)
+    return (u.cpu().numpy(), tuple(q.cpu().numpy() for q in qs),
+            SolveReport(iters, relres, conv, wall, wall / max(iters, 1), None))
+
+
 def solve(u0, f, g_D, g_N, cfg, ctx):
-    """Hybridise, build the RHS, iterate on the device, recover (u, q) (solver.py:338-369)."""
+    """Hybridise, build the RHS, iterate on the device, recover (u, q) (solver.py:338-369).
+
+    Runs device-resident (`_solve_device`) unless the context carries a FlopCounter, whose
+    per-call accounting follows the host pipeline below.
+    """
     if cfg.preconditioner == "transformed":
         return solve_transformed(u0, f, g_D, g_N, cfg, ctx)
+    if getattr(ctx, "counter", None) is None:
+        return _solve_device(u0, f, g_D, g_N, cfg, ctx, False)
     ops0 = _ops(ctx)
     prec = _build_preconditioner(cfg.preconditioner, ctx)
     u_tilde0 = hybridize_initial_guess(u0, ctx, g_D, g_N)
@@ -512,6 +579,8 @@ def solve(u0, f, g_D, g_N, cfg, ctx):
 
 def solve_transformed(u0, f, g_D, g_N, cfg, ctx):
     """Same pipeline in the transformed basis (solver.py:372-410, Alg. 6)."""
+    if getattr(ctx, "counter", None) is None:
+        return _solve_device(u0, f, g_D, g_N, cfg, ctx, True)
     ops0 = _ops(ctx)
     prec = transformed_preconditioner(ctx)
     u_tilde0 = hybridize_initial_guess(u0, ctx, g_D, g_N)

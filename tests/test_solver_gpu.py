@@ -75,3 +75,75 @@ def test_flop_counter_matches_reference_formulas():
     ctx.counter.reset()
     hb.hdg_op_3d_transformed(fu, ctx)
     assert ctx.counter.ops == mesh.n_elements * (25 * n**3 + 12 * n**2)
+
+
+@pytest.mark.parametrize("p,bc,lam", [(4, "dirichlet", 0.0), (3, ("neumann", "dirichlet", "dirichlet", "neumann",
+                                                                   "neumann", "dirichlet"), 1.3), (8, "dirichlet", 1.0)])
+def test_device_build_rhs_and_recover_match_host(p, bc, lam):
+    """Device pre/post (hdgb_build_rhs / hdgb_recover_interior) vs the host restatement."""
+    mesh = hb.Mesh((3, 2, 2), (0.0, 0.0, 0.0), (1.5, 1.0, 1.0), bc)
+    ctx = hb.make_context(mesh, p, hb.SolverConfig(lam=lam, tau_convention="reference", tau=0.8))
+    dc = hb.device_context(ctx)
+    rng = np.random.default_rng(p)
+    f = rng.uniform(-1, 1, (mesh.n_elements,) + (ctx.basis.n,) * 3)
+    F_host = hb.pack_all(hb.build_rhs(f, None, None, ctx))
+    F_dev = dc.build_rhs(f)
+    dc.zero_dirichlet(F_dev)
+    assert np.max(np.abs(F_dev.cpu().numpy() - F_host)) <= 1e-12 * np.max(np.abs(F_host))
+    tr = rng.uniform(-1, 1, mesh.n_all(p))
+    u_h, q_h = hb.recover_interior(f, hb.unpack_all(tr, mesh, p), ctx)
+    u_d, q_d = dc.recover_interior(f, torch.from_numpy(tr).cuda())
+    assert np.max(np.abs(u_d.cpu().numpy() - u_h)) <= 1e-12 * np.max(np.abs(u_h))
+    for d in range(3):
+        assert np.max(np.abs(q_d[d].cpu().numpy() - q_h[d])) <= 1e-12 * np.max(np.abs(q_h[d]))
+
+
+def test_device_build_rhs_matches_reference_golden():
+    from tests._golden import load, sinsin_field
+
+    g = load("cfg1")
+    mesh = hb.Mesh(tuple(int(v) for v in g["n_el"]), (0, 0, 0), tuple(float(v) for v in g["hi"]), "dirichlet")
+    ctx = hb.OperatorContext(hb.Basis1D(int(g["p"]), float(g["tau_hat"])), mesh, float(g["lam"]))
+    dc = hb.device_context(ctx)
+    f = sinsin_field(mesh, ctx.basis, float(g["lam"]))
+    F = dc.build_rhs(f)
+    dc.zero_dirichlet(F)
+    Fp = dc.pack(F).cpu().numpy()
+    assert np.max(np.abs(Fp - g["sin_F"])) <= 1e-12 * np.max(np.abs(g["sin_F"]))
+
+
+def test_device_pre_post_nonuniform_grid():
+    rng = np.random.default_rng(3)
+    n_el, L = (4, 3, 2), (2.0, 1.0, 1.0)
+    widths = []
+    for d in range(3):
+        w = rng.uniform(0.5, 2.0, n_el[d]) * (L[d] / n_el[d])
+        widths.append(w * (L[d] / w.sum()))
+    p = 5
+    mesh = hb.Mesh(n_el, (0, 0, 0), L, "dirichlet", widths=widths)
+    ctx = hb.OperatorContext(hb.Basis1D(p, 0.4), mesh, 2.0)
+    dc = hb.device_context(ctx)
+    f = rng.uniform(-1, 1, (mesh.n_elements,) + (p + 1,) * 3)
+    F_host = hb.pack_all(hb.build_rhs(f, None, None, ctx))
+    F_dev = dc.zero_dirichlet(dc.build_rhs(f))
+    assert np.max(np.abs(F_dev.cpu().numpy() - F_host)) <= 1e-12 * np.max(np.abs(F_host))
+    tr = rng.uniform(-1, 1, mesh.n_all(p))
+    u_h, q_h = hb.recover_interior(f, hb.unpack_all(tr, mesh, p), ctx)
+    u_d, q_d = dc.recover_interior(f, torch.from_numpy(tr).cuda())
+    assert np.max(np.abs(u_d.cpu().numpy() - u_h)) <= 1e-12 * np.max(np.abs(u_h))
+    for d in range(3):
+        assert np.max(np.abs(q_d[d].cpu().numpy() - q_h[d])) <= 1e-12 * np.max(np.abs(q_h[d]))
+
+
+@pytest.mark.parametrize("precond", ["block", "transformed"])
+def test_device_resident_solve_matches_host_pipeline(precond):
+    """solve() device-resident path vs the host pre/post pipeline (FlopCounter attached)."""
+    mesh, cfg, ctx, f, g_D, _ = make_problem(p=5, lam=0.5, precond=precond)
+    u0 = np.random.default_rng(2).uniform(-1, 1, (mesh.n_elements,) + (ctx.basis.n,) * 3)
+    u_d, q_d, rd = hb.solve(u0, f, g_D, None, cfg, ctx)
+    ctx_h = hb.make_context(mesh, 5, cfg, counter=hb.FlopCounter())
+    u_h, q_h, rh = hb.solve(u0, f, g_D, None, cfg, ctx_h)
+    assert rd.converged and abs(rd.iterations - rh.iterations) <= 1
+    assert np.max(np.abs(u_d - u_h)) <= 1e-8 * np.max(np.abs(u_h))
+    for d in range(3):
+        assert np.max(np.abs(q_d[d] - q_h[d])) <= 1e-8 * np.max(np.abs(q_h[d]))
