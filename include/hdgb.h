@@ -117,8 +117,14 @@ int hdgb_pcg(hdgb_ctx* ctx, int variant, int prec, const double* F, double* x, d
 
 /* ---- element-local pre/post of the condensed solve ----
  * Reference-element tables of the interior solver: D = M Dhat (n*n, row-major), B and C
- * (n*2, row-major), host pointers (basis.py:96-120).  Required by the two calls below. */
-int hdgb_ctx_set_element_tables(hdgb_ctx* ctx, const double* D, const double* B, const double* C);
+ * (n*2, row-major), host pointers, and the reference penalty tau_hat (basis.py:96-120).
+ * Required by the three calls below. */
+int hdgb_ctx_set_element_tables(hdgb_ctx* ctx, const double* D, const double* B, const double* C, double tau_hat);
+/* x (all faces) = hybridize_initial_guess (solver.py:158-195) of the element field u0
+ * (n_e * n^3): 0.5 u - (q.n)/(2 tau) summed over the adjacent elements, Neumann faces
+ * u - (q.n - g_N)/tau (g_N: all-face vector or NULL for zero data), Dirichlet faces 0 (the
+ * caller adds g_D). */
+int hdgb_hybridize(hdgb_ctx* ctx, const double* u0, const double* g_N, double* x, void* stream);
 /* F (all faces) = element part of build_rhs (solver.py:212-251): -sum over elements of the flux
  * couplings of A^-1 (M3 f, 0), Dirichlet faces included (the caller adds Neumann data, subtracts
  * the Dirichlet lift K g_D and zeroes Dirichlet rows).  f: n_e * n^3 element values

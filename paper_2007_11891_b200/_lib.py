@@ -63,7 +63,8 @@ SIGNATURES = {
                                ctypes.POINTER(_I32), ctypes.POINTER(_D), ctypes.POINTER(_I32), _VP]),
     "hdgb_dot_scratch_doubles": (_I64, []),
     "hdgb_vec_dot": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
-    "hdgb_ctx_set_element_tables": (ctypes.c_int, [_VP, _VP, _VP, _VP]),
+    "hdgb_ctx_set_element_tables": (ctypes.c_int, [_VP, _VP, _VP, _VP, _D]),
+    "hdgb_hybridize": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "hdgb_build_rhs": (ctypes.c_int, [_VP, _VP, _VP, _VP]),
     "hdgb_recover_interior": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
     "hdgb_face_dot": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),

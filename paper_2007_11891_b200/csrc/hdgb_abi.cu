@@ -392,12 +392,22 @@ int hdgb_vec_dot(const double* x, const double* y, int64_t n, double* scratch, d
   return HDGB_OK;
 }
 
-int hdgb_ctx_set_element_tables(hdgb_ctx* c, const double* D, const double* B, const double* C) {
+int hdgb_ctx_set_element_tables(hdgb_ctx* c, const double* D, const double* B, const double* C, double tau_hat) {
   if (!c || !D || !B || !C) return einval("null argument");
+  if (!(tau_hat > 0.0)) return einval("tau_hat must be positive");
   const int N = c->N;
   c->h_elem.assign(D, D + N * N);
   c->h_elem.insert(c->h_elem.end(), B, B + 2 * N);
   c->h_elem.insert(c->h_elem.end(), C, C + 2 * N);
+  c->h_elem.push_back(tau_hat);
+  return HDGB_OK;
+}
+
+int hdgb_hybridize(hdgb_ctx* c, const double* u0, const double* gN, double* x, void* stream) {
+  if (!c || !u0 || !x) return einval("null argument");
+  if (c->h_elem.empty()) return einval("element tables not set (hdgb_ctx_set_element_tables)");
+  if (c->g.ne == 0) return HDGB_OK;
+  HDGB_CUDA(launch_hybridize(c, u0, gN, x, (cudaStream_t)stream));
   return HDGB_OK;
 }
 

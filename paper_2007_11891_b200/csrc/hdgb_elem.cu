@@ -26,6 +26,8 @@ struct ElemConst {
   double BDC[2 * N]; // recovery volume term [a][s]
   double C[2 * N];   // C[a][s]
   double w[N];       // quadrature weights
+  double Dh[N * N];  // Dhat = M^-1 D (nodal derivative)
+  double tau_hat;    // reference-element penalty
 };
 
 template <int N>
@@ -232,10 +234,13 @@ static ElemConst<N> elem_const(const hdgb_ctx* c) {
   to.set(N);
   for (int q = 0; q < N * N; ++q) K.S[q] = c->h_tab[to.S + q];
   for (int i = 0; i < N; ++i) K.w[i] = c->h_tab[to.w + i];
-  const std::vector<double>& E = c->h_elem;  // D (N*N), B (N*2), C (N*2)
+  const std::vector<double>& E = c->h_elem;  // D (N*N), B (N*2), C (N*2), tau_hat
   const double* D = E.data();
   const double* B = D + N * N;
   const double* Cm = B + 2 * N;
+  K.tau_hat = Cm[2 * N];
+  for (int i = 0; i < N; ++i)
+    for (int k = 0; k < N; ++k) K.Dh[i * N + k] = D[i * N + k] / K.w[i];
   // MD = M^-1 D^T : MD[i][k] = D[k][i] / w[i]
   for (int i = 0; i < N; ++i)
     for (int k = 0; k < N; ++k) K.MD[i * N + k] = D[k * N + i] / K.w[i];
@@ -255,6 +260,67 @@ static ElemConst<N> elem_const(const hdgb_ctx* c) {
       K.C[a2 * 2 + s] = Cm[a2 * 2 + s];
     }
   return K;
+}
+
+// hybridize_initial_guess (solver.py:158-195): trace = 0.5 u - (q.n)/(2 tau) summed over the
+// adjacent elements (two colour passes), Neumann faces u - (q.n - g_N)/tau, Dirichlet faces 0
+// (the caller adds g_D); tau = (2/h_d) tau_hat, the mean over the two sides on non-uniform grids.
+template <int N, int COLOR, int UNI>
+__global__ void __launch_bounds__(ElemCfg<N>::NT) hyb_kernel(const OpArgs a, const double* __restrict__ u0,
+                                                           const double* __restrict__ gN, int64_t npairs,
+                                                           const __grid_constant__ ElemConst<N> K) {
+  using C = ElemCfg<N>;
+  constexpr int NQ = C::NQ;
+  extern __shared__ __align__(16) double smem[];
+  double* vol = smem;
+  const int t = threadIdx.x;
+  const bool on = t < NQ;
+  const int t1 = t / N, t2 = t - (t / N) * N;
+  const Geo& g = a.g;
+  for (int64_t pi = blockIdx.x; pi < npairs; pi += gridDim.x) {
+    Elem E;
+    if (!pair_elem(g, pi, COLOR, E)) continue;
+    const int64_t e = E.c[0] + (int64_t)g.n1 * (E.c[1] + (int64_t)g.n2 * E.c[2]);
+    __syncthreads();
+    for (int q = t; q < N * NQ; q += blockDim.x) vol[q] = u0[e * N * NQ + q];
+    __syncthreads();
+    if (!on) continue;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int nd = d == 0 ? g.n1 : (d == 1 ? g.n2 : g.n3);
+      const int off = d == 0 ? 0 : (d == 1 ? g.n1 : g.n1 + g.n2);
+      const double two_h = 2.0 / a.widths[off + E.c[d]];
+      double x[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+        x[k] = vol[d == 0 ? vidx<N, 0>(k, t1, t2) : (d == 1 ? vidx<N, 1>(k, t1, t2) : vidx<N, 2>(k, t1, t2))];
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int s = 2 * d + side, ia = side ? N - 1 : 0, plane = E.c[d] + side;
+        double dq = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) dq = fma(K.Dh[ia * N + k], x[k], dq);
+        const double qn = (side ? 1.0 : -1.0) * two_h * dq;  // outward normal flux
+        const int kind = face_kind(g, d, plane);
+        double tau = two_h;
+        if (!UNI && plane > 0 && plane < nd) {  // interior face: mean over both elements
+          const int other = E.c[d] + (side ? 1 : -1);
+          tau = 0.5 * (two_h + 2.0 / a.widths[off + other]);
+        }
+        tau *= K.tau_hat;
+        const int64_t gi = E.fid[s] * NQ + t;
+        double val = 0.5 * x[ia] - qn / (2.0 * tau);
+        if (kind == HDGB_NEUMANN) {
+          val = x[ia] - (qn - (gN ? gN[gi] : 0.0)) / tau;
+        } else if (kind == HDGB_DIRICHLET) {
+          val = 0.0;
+        } else if (COLOR == 1 && (E.shared >> s & 1u)) {
+          val = __ldcg(a.r + gi) + val;
+        }
+        a.r[gi] = val;
+      }
+    }
+  }
 }
 
 static OpArgs elem_args(hdgb_ctx* c) {
@@ -301,6 +367,37 @@ static cudaError_t launch_rhs_n(hdgb_ctx* c, const double* f, double* F, cudaStr
 }
 
 template <int N>
+static cudaError_t launch_hyb_n(hdgb_ctx* c, const double* u0, const double* gN, double* x, cudaStream_t s) {
+  using C = ElemCfg<N>;
+  const ElemConst<N> K = elem_const<N>(c);
+  OpArgs a = elem_args(c);
+  a.r = x;
+  const size_t smem = sizeof(double) * N * C::NQ;
+  const int64_t npairs = (int64_t)((c->g.n1 + 1) / 2) * c->g.n2 * c->g.n3;
+  for (int color = 0; color < 2; ++color) {
+    static int cache[2][2][16] = {};
+    int64_t grid = 0;
+    cudaError_t e;
+    if (c->uniform) {
+      auto k = color ? hyb_kernel<N, 1, 1> : hyb_kernel<N, 0, 1>;
+      if ((e = resident_grid(k, C::NT, smem, c->dev, cache[1][color], &grid)) != cudaSuccess) return e;
+      if (grid > npairs) grid = npairs;
+      if (grid < 1) return cudaSuccess;
+      k<<<(unsigned)grid, C::NT, smem, s>>>(a, u0, gN, npairs, K);
+    } else {
+      auto k = color ? hyb_kernel<N, 1, 0> : hyb_kernel<N, 0, 0>;
+      if ((e = resident_grid(k, C::NT, smem, c->dev, cache[0][color], &grid)) != cudaSuccess) return e;
+      if (grid > npairs) grid = npairs;
+      if (grid < 1) return cudaSuccess;
+      k<<<(unsigned)grid, C::NT, smem, s>>>(a, u0, gN, npairs, K);
+    }
+    c->launches++;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+template <int N>
 static cudaError_t launch_recover_n(hdgb_ctx* c, const double* f, const double* tr, double* u, double* q,
                                    cudaStream_t s) {
   using C = ElemCfg<N>;
@@ -332,6 +429,19 @@ cudaError_t launch_build_rhs(hdgb_ctx* c, const double* f, double* F, cudaStream
 #define HDGB_CASE(n) \
   case n:            \
     return launch_rhs_n<n>(c, f, F, s);
+    HDGB_CASE(2) HDGB_CASE(3) HDGB_CASE(4) HDGB_CASE(5) HDGB_CASE(6) HDGB_CASE(7) HDGB_CASE(8) HDGB_CASE(9)
+    HDGB_CASE(10) HDGB_CASE(11) HDGB_CASE(12) HDGB_CASE(13) HDGB_CASE(14) HDGB_CASE(15) HDGB_CASE(16)
+    HDGB_CASE(17)
+#undef HDGB_CASE
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_hybridize(hdgb_ctx* c, const double* u0, const double* gN, double* x, cudaStream_t s) {
+  switch (c->N) {
+#define HDGB_CASE(n) \
+  case n:            \
+    return launch_hyb_n<n>(c, u0, gN, x, s);
     HDGB_CASE(2) HDGB_CASE(3) HDGB_CASE(4) HDGB_CASE(5) HDGB_CASE(6) HDGB_CASE(7) HDGB_CASE(8) HDGB_CASE(9)
     HDGB_CASE(10) HDGB_CASE(11) HDGB_CASE(12) HDGB_CASE(13) HDGB_CASE(14) HDGB_CASE(15) HDGB_CASE(16)
     HDGB_CASE(17)

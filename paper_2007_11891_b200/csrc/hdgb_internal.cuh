@@ -258,7 +258,7 @@ struct hdgb_ctx {
   double* d_facedot = nullptr;
   double* d_part = nullptr;
   std::vector<double> h_tab;      // host copy of d_tab (1D matrices become kernel parameters)
-  std::vector<double> h_elem;     // pre/post tables D (n*n), B (n*2), C (n*2); empty until set
+  std::vector<double> h_elem;     // pre/post tables D (n*n), B (n*2), C (n*2), tau_hat; empty until set
   double* d_fcoef = nullptr;      // per-face self-term coefficient sum_sides alpha_d GCC_ll
   double* d_hat = nullptr;        // plain operator: eigen-space input (T (x) T) u  (n_all)
   hdgb::CGState* d_st = nullptr;
@@ -286,6 +286,7 @@ cudaError_t launch_op(hdgb_ctx* c, int variant, int mode, const double* u, doubl
 cudaError_t launch_face_transform(hdgb_ctx* c, const double* A_host, const double* in, double* out, cudaStream_t s);
 cudaError_t launch_plain_post(hdgb_ctx* c, int cg, const double* u, double* r, cudaStream_t s);
 cudaError_t launch_build_rhs(hdgb_ctx* c, const double* f, double* F, cudaStream_t s);
+cudaError_t launch_hybridize(hdgb_ctx* c, const double* u0, const double* gN, double* x, cudaStream_t s);
 cudaError_t launch_recover(hdgb_ctx* c, const double* f, const double* tr, double* u, double* q, cudaStream_t s);
 cudaError_t launch_prec(hdgb_ctx* c, int kind, const double* in, double* out, cudaStream_t s);
 cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s);

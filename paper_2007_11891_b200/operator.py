@@ -189,7 +189,8 @@ class DeviceContext:
         self.handle = handle
         # reference-element tables of the interior solver (device build_rhs / recover_interior)
         Dm, Bm, Cm = (np.ascontiguousarray(getattr(basis, k), dtype=np.float64) for k in ("D", "B", "C"))
-        _lib.check(L.hdgb_ctx_set_element_tables(handle, _lib.dptr(Dm), _lib.dptr(Bm), _lib.dptr(Cm)))
+        _lib.check(L.hdgb_ctx_set_element_tables(handle, _lib.dptr(Dm), _lib.dptr(Bm), _lib.dptr(Cm),
+                                                 float(basis.tau_hat)))
         self.n_all = int(L.hdgb_ctx_n_all(handle))
         self.n_unknown = int(L.hdgb_ctx_n_unknown(handle))
         self._scratch = None
@@ -271,6 +272,19 @@ class DeviceContext:
         _lib.check(_lib.lib().hdgb_build_rhs(self.handle, ctypes.c_void_p(f.data_ptr()), self.check_vec(F),
                                              self.stream()))
         return F
+
+    def hybridize(self, u0, g_N=None):
+        """All-face trace of hybridize_initial_guess (solver.py:158-195); Dirichlet faces 0."""
+        import torch
+
+        u0 = torch.as_tensor(u0, dtype=torch.float64).to(f"cuda:{self.device}").contiguous()
+        if u0.numel() != self.mesh.n_elements * self.n ** 3:
+            raise ValueError("u0 must hold n_elements * (p+1)^3 values")
+        x = self.empty()
+        gp = ctypes.c_void_p(None) if g_N is None else self.check_vec(g_N)
+        _lib.check(_lib.lib().hdgb_hybridize(self.handle, ctypes.c_void_p(u0.data_ptr()), gp, self.check_vec(x),
+                                             self.stream()))
+        return x
 
     def recover_interior(self, f, trace):
         """(u, (q1, q2, q3)) from f and the all-face trace (solver.py:254-279), device tensors."""

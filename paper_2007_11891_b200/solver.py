@@ -497,8 +497,8 @@ _PREC_KIND = {"none": _lib.PREC_NONE, "diagonal": _lib.PREC_DIAG_NODAL, "block":
 def _solve_device(u0, f, g_D, g_N, cfg, ctx, transformed):
     """Device-resident solve: element RHS, fused PCG and interior recovery on the GPU.
 
-    Host work is limited to the boundary data (Neumann face masses, the Dirichlet lift
-    vector) and a non-zero initial guess (hybridize_initial_guess).
+    Host work is limited to packing the boundary data (Neumann data and face masses, the
+    Dirichlet lift vector).
     """
     import torch
 
@@ -524,11 +524,14 @@ def _solve_device(u0, f, g_D, g_N, cfg, ctx, transformed):
             lift = torch.from_numpy(pack_all(lf)).to(dev)
             F -= dc.apply(lift, _lib.PLAIN)
     dc.zero_dirichlet(F)
-    u0a = np.asarray(u0, dtype=float)
-    if np.any(u0a) or g_D is not None or g_N is not None:
-        x = torch.from_numpy(pack_all(hybridize_initial_guess(u0a, ctx, g_D, g_N))).to(dev)
-    else:
-        x = torch.zeros(dc.n_all, dtype=torch.float64, device=dev)
+    gN = None
+    if g_N is not None:
+        gf = FluxField(mesh, p)
+        for d in range(3):
+            m = mesh.face_kind[d] == NEUMANN
+            gf.data[d][m] = g_N.data[d][m]
+        gN = torch.from_numpy(pack_all(gf)).to(dev)
+    x = dc.hybridize(u0, gN)  # Dirichlet slots 0: the PCG keeps them there, the lift restores them
     if transformed:  # Alg. 6: solve in the eigenbasis (solver.py:381-399)
         F = dc.zero_dirichlet(dc.transform(F, np.ascontiguousarray(ctx.basis.S.T)))
         x = dc.transform(x, np.ascontiguousarray(ctx.T))

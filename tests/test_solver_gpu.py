@@ -147,3 +147,34 @@ def test_device_resident_solve_matches_host_pipeline(precond):
     assert np.max(np.abs(u_d - u_h)) <= 1e-8 * np.max(np.abs(u_h))
     for d in range(3):
         assert np.max(np.abs(q_d[d] - q_h[d])) <= 1e-8 * np.max(np.abs(q_h[d]))
+
+
+@pytest.mark.parametrize("uniform", [True, False])
+def test_device_hybridize_matches_host(uniform):
+    rng = np.random.default_rng(8)
+    n_el, L = (3, 2, 3), (1.5, 1.0, 1.5)
+    bc = ("neumann", "dirichlet", "neumann", "dirichlet", "dirichlet", "neumann")
+    widths = None
+    if not uniform:
+        widths = []
+        for d in range(3):
+            w = rng.uniform(0.5, 2.0, n_el[d]) * (L[d] / n_el[d])
+            widths.append(w * (L[d] / w.sum()))
+    p = 4
+    mesh = hb.Mesh(n_el, (0, 0, 0), L, bc, widths=widths)
+    ctx = hb.OperatorContext(hb.Basis1D(p, 0.7), mesh, 0.3)
+    dc = hb.device_context(ctx)
+    u0 = rng.uniform(-1, 1, (mesh.n_elements,) + (p + 1,) * 3)
+    g_N = hb.FluxField(mesh, p)
+    for d in range(3):
+        g_N.data[d][...] = rng.uniform(-1, 1, g_N.data[d].shape)
+    host = hb.hybridize_initial_guess(u0, ctx, None, g_N)
+    hv = hb.pack_all(host)
+    gn_all = hb.FluxField(mesh, p)
+    for d in range(3):
+        m = mesh.face_kind[d] == hb.NEUMANN
+        gn_all.data[d][m] = g_N.data[d][m]
+    dv = dc.hybridize(u0, torch.from_numpy(hb.pack_all(gn_all)).cuda()).cpu().numpy()
+    unk = np.concatenate([np.repeat(mesh.face_kind[d] != hb.DIRICHLET, (p + 1) ** 2) for d in range(3)])
+    assert np.max(np.abs(dv[unk] - hv[unk])) <= 1e-12 * np.max(np.abs(hv))
+    assert np.all(dv[~unk] == 0.0)
