@@ -28,6 +28,14 @@ int cuda_fail(cudaError_t e, const char* what) {
   g_err = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
   return HDGB_ECUDA;
 }
+bool pdl_enabled() {
+  static const int on = [] {
+    const char* v = getenv("HDGB_PDL");
+    return v ? atoi(v) : 1;
+  }();
+  return on != 0;
+}
+
 static int einval(const std::string& m) {
   g_err = m;
   return HDGB_EINVAL;

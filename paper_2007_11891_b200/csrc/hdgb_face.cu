@@ -36,6 +36,8 @@ constexpr int PW_GRID = 1184; // fixed grid (8 CTAs x 148 SMs)
 template <int N, int PREC, int FK, bool WITHZ>
 __global__ void __launch_bounds__(256) pw_kernel(FaceArgs a, const uint8_t* __restrict__ finfo, unsigned n) {
   constexpr unsigned N2 = N * N;
+  pdl_trigger();
+  pdl_wait();
   if (FK != PW_PREC && a.st->done) return;
   const double alpha = FK == PW_UPDATE ? a.st->alpha : 0.0;
   double rr = 0.0, rz = 0.0;
@@ -239,7 +241,11 @@ __global__ void __launch_bounds__(FxCfg<N, FK>::NT, (FxCfg<N, FK>::MINB)) fx_ker
   constexpr bool RED = FK == FX_INIT || FK == FX_UPDATE;
   constexpr bool POST = FK == FX_POST;
   constexpr bool ODD = N & 1;  // row-wise stores N doubles apart are bank-conflict-free
-  if ((RED || (POST && CG)) && a.st->done) return;
+  pdl_trigger();
+  if (RED || (POST && CG)) {
+    pdl_wait();
+    if (a.st->done) return;
+  }
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t sBar[C::NG][S];
   __shared__ double sWq[N];  // FX_POST: quadrature weights (dynamic index: keep out of the constant bank)
@@ -258,6 +264,7 @@ __global__ void __launch_bounds__(FxCfg<N, FK>::NT, (FxCfg<N, FK>::MINB)) fx_ker
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();  // the only CTA-wide barrier: tables and barrier init
+  if (!(RED || (POST && CG))) pdl_wait();  // inputs come from earlier kernels
   auto gsync = [&]() {
     if (GW == 1) {
       __syncwarp();
@@ -424,6 +431,8 @@ __global__ void __launch_bounds__(FxCfg<N, FK>::NT, (FxCfg<N, FK>::MINB)) fx_ker
 // <p, w> from the per-face dots of the operator kernel -> alpha (solver.py:303-310)
 __global__ void __launch_bounds__(HDGB_NT) reduce_pw_kernel(const double* __restrict__ facedot, int64_t nf,
                                                             double* part, CGState* st) {
+  pdl_trigger();
+  pdl_wait();
   if (st->done) return;
   double s = 0.0, dummy = 0.0;
   const int64_t per = (nf + gridDim.x - 1) / gridDim.x;
@@ -743,9 +752,9 @@ static cudaError_t pw_launch(hdgb_ctx* c, const FaceArgs& a, cudaStream_t s) {
   const int64_t n = c->n_all;
   int grid = (int)min((int64_t)PW_GRID, (n + 256 * PW_U - 1) / (256 * PW_U));
   if (grid < 1) grid = 1;
-  pw_kernel<N, PREC, FK, WITHZ><<<grid, 256, 0, s>>>(a, c->d_finfo, (unsigned)n);
+  cudaError_t le = launch_pdl(pw_kernel<N, PREC, FK, WITHZ>, dim3(grid), dim3(256), 0, s, a, c->d_finfo, (unsigned)n);
   c->launches++;
-  return cudaGetLastError();
+  return le;
 }
 
 template <int N, int FK, bool WITHZ>
@@ -781,9 +790,9 @@ static cudaError_t fx_launch(hdgb_ctx* c, const FaceArgs& a, const double* Ah, c
   if (grid > PW_GRID) grid = PW_GRID;
   if (grid > nb) grid = nb;
   if (grid < 1) grid = 1;
-  k<<<(unsigned)grid, C::NT, smem, s>>>(a, c->d_finfo, c->d_fcoef, M);
+  cudaError_t le = launch_pdl(k, dim3((unsigned)grid), dim3(C::NT), smem, s, a, c->d_finfo, c->d_fcoef, M);
   c->launches++;
-  return cudaGetLastError();
+  return le;
 }
 
 template <int N, int FK>
@@ -921,9 +930,10 @@ cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s) {
 
 cudaError_t launch_reduce_pw(hdgb_ctx* c, cudaStream_t s) {
   int grid = (int)min((int64_t)HDGB_RED_BLOCKS, max((int64_t)1, c->nfaces / 64));
-  reduce_pw_kernel<<<grid, HDGB_NT, 0, s>>>(c->d_facedot, c->nfaces, c->d_part, c->d_st);
+  cudaError_t le = launch_pdl(reduce_pw_kernel, dim3(grid), dim3(HDGB_NT), 0, s, (const double*)c->d_facedot,
+                              c->nfaces, c->d_part, c->d_st);
   c->launches++;
-  return cudaGetLastError();
+  return le;
 }
 
 cudaError_t launch_p_update(hdgb_ctx* c, cudaStream_t s, cudaGraphConditionalHandle loop, int has_loop) {

@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/hdgb.h"
@@ -298,6 +299,30 @@ cudaError_t op_set_smem_limits(hdgb_ctx* c);
 }  // namespace hdgb
 
 namespace hdgb {
+// ---- programmatic dependent launch (PDL): a kernel launched with launch_pdl may start while
+// the previous kernel in the stream drains; it runs its prologue (constant tables, barrier
+// init, element geometry) and calls pdl_wait() before touching anything an earlier kernel
+// wrote.  Every kernel triggers its dependents at entry.  HDGB_PDL=0 disables the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 // Resident CTAs x SMs of a kernel with `smem` dynamic shared memory on device `dev`, with its
 // shared-memory limit raised once per device.  `Cache` is a per-kernel static (the host
 // launch path is otherwise dominated by attribute queries at small problem sizes).

@@ -138,7 +138,11 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
   using C = OpVCfg<N>;
   constexpr int NQ = C::NQ, G = C::G, FS = C::FS, VS = C::VS;
   constexpr bool UNI = !(MODE & 2), CG = MODE & 1, GONLY = MODE & 4;
-  if (CG && a.st->done) return;
+  pdl_trigger();
+  if (CG) {
+    pdl_wait();
+    if (a.st->done) return;
+  }
   extern __shared__ __align__(16) double smem[];
   double* sF0 = smem;              // 2 x G x [6][NQ] staged faces
   double* sU = smem + 2 * G * FS;  // G x [N][NQ] volume
@@ -195,6 +199,7 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
   int64_t gi = blockIdx.x;
   if (gi < ngroups) info(gi, sInfo[0]);
   __syncthreads();
+  if (!CG) pdl_wait();  // u and r come from earlier kernels
   if (gi < ngroups) stage(sInfo[0], sF0);
   cp_async_commit();
   for (int buf = 0; gi < ngroups; gi += gridDim.x, buf ^= 1) {
@@ -322,9 +327,9 @@ static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
     K.B1[q] = c->h_tab[to.BS + 2 * q + 1];
     K.Lam[q] = c->h_tab[to.Lam + q];
   }
-  kern<<<(unsigned)grid, Cf::NT, smem, s>>>(a, t0, t1, K);
+  cudaError_t le = launch_pdl(kern, dim3((unsigned)grid), dim3(Cf::NT), smem, s, a, t0, t1, K);
   c->launches++;
-  return cudaGetLastError();
+  return le;
 }
 
 template <int N, bool PLAIN, int MODE, int COLOR>
