@@ -10,7 +10,6 @@
 
 namespace hdgb {
 cudaError_t launch_cg_init(hdgb_ctx* c, int kind, cudaStream_t s);
-cudaError_t launch_reduce_pw(hdgb_ctx* c, cudaStream_t s);
 cudaError_t launch_p_update(hdgb_ctx* c, cudaStream_t s, cudaGraphConditionalHandle loop, int has_loop);
 cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* scratch, double* result, cudaStream_t s);
 cudaError_t launch_face_dot(hdgb_ctx* c, const double* x, const double* y, double* scratch, double* result,
@@ -64,7 +63,7 @@ static void free_ctx(hdgb_ctx* c) {
     for (auto& gx : row)
       if (gx) cudaGraphExecDestroy(gx);
   double* bufs[] = {c->d_tab, c->d_dz, c->d_widths, c->d_yinv_cls, c->d_y_cls, c->d_dn_cls, c->d_yinv_full,
-                    c->d_y_full, c->d_dn_full, c->d_hat, c->d_facedot, c->d_part, c->d_fcoef, c->d_vec, c->d_io};
+                    c->d_y_full, c->d_dn_full, c->d_hat, c->d_part, c->d_fcoef, c->d_vec, c->d_io};
   for (double* b : bufs)
     if (b) cudaFree(b);
   if (c->d_finfo) cudaFree(c->d_finfo);
@@ -240,7 +239,6 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
     CK(cudaMalloc(&c->d_fcoef, sizeof(double) * (c->nfaces > 0 ? c->nfaces : 1)));
     CK(cudaMemcpy(c->d_fcoef, fcoef.data(), sizeof(double) * c->nfaces, cudaMemcpyHostToDevice));
   }
-  CK(cudaMalloc(&c->d_facedot, sizeof(double) * c->nfaces));
   CK(cudaMalloc(&c->d_part, sizeof(double) * 4 * HDGB_RED_BLOCKS + 64));
   CK(cudaMalloc(&c->d_st, sizeof(CGState)));
   CK(cudaMemset(c->d_st, 0, sizeof(CGState)));
@@ -331,15 +329,6 @@ int hdgb_prec_apply(hdgb_ctx* c, int kind, const double* r, double* z, void* str
   if (kind < HDGB_PREC_NONE || kind > HDGB_PREC_DIAG_EIGEN) return einval("unknown preconditioner kind");
   if (!al16(r) || !al16(z)) return einval("device vectors must be 16-byte aligned");
   HDGB_CUDA(launch_prec(c, kind, r, z, (cudaStream_t)stream));
-  return HDGB_OK;
-}
-
-// debug hook (not part of the public header): CG-mode operator + per-face dots
-int hdgb_debug_op_cg(hdgb_ctx* c, int variant, const double* u, double* r, double* facedot_out, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
-  HDGB_CUDA(cudaMemsetAsync(c->d_st, 0, sizeof(CGState), s));
-  HDGB_CUDA(launch_op(c, variant, MODE_CG, u, r, s));
-  HDGB_CUDA(cudaMemcpyAsync(facedot_out, c->d_facedot, sizeof(double) * c->nfaces, cudaMemcpyDeviceToDevice, s));
   return HDGB_OK;
 }
 
@@ -457,8 +446,8 @@ static cudaError_t enqueue_iteration(hdgb_ctx* c, int variant, int prec, cudaGra
   double* v = c->d_vec;
   const int64_t n = c->n_all;
   cudaError_t e;
-  if ((e = launch_op(c, variant, MODE_CG, v + V_P * c->vstride, v + V_W * c->vstride, c->s)) != cudaSuccess) return e;  // w = K p, <p,w>
-  if ((e = launch_reduce_pw(c, c->s)) != cudaSuccess) return e;                                      // alpha
+  // w = K p with <p, w> and alpha finished by the operator's last kernel
+  if ((e = launch_op(c, variant, MODE_CG, v + V_P * c->vstride, v + V_W * c->vstride, c->s)) != cudaSuccess) return e;
   if ((e = launch_cg_update(c, prec, c->s)) != cudaSuccess) return e;  // x,r update; z = P r; ||r||, <r,z>
   return launch_p_update(c, c->s, h, has_loop);                        // p = z + beta p; loop control
 }

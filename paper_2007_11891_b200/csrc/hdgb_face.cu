@@ -392,26 +392,25 @@ __global__ void __launch_bounds__(FxCfg<N, FK>::NT, (FxCfg<N, FK>::MINB)) fx_ker
         // r = (sum_sides alpha_d GCC_ll) (w (x) w) u - (MS (x) MS) G
         const double u0 = uv[POST ? m : 0];
         v = ((__ldg(fcoef + f0 + fi) * sWq[j]) * sWq[kk]) * u0 - v;
-        if (CG) {
+        if (CG) {  // final w: Dirichlet row -> 0, <p, w> (p = u here)
           const int kind = finfo_kind(__ldg(finfo + f0 + fi));
           if (kind == HDGB_DIRICHLET) v = 0.0;
-          sX[it] = kind_counts(kind) ? u0 * v : 0.0;  // ODD: own slot; even: the stage is consumed
+          if (kind_counts(kind)) rz = fma(u0, v, rz);
         }
       }
       a.out[gi] = v;
       if (FK == FX_INIT) a.p[gi] = v;
     }
-    if (POST && CG) {  // per-face <u, r>, fixed order; warp w of the group takes faces w, w+GW, ...
-      gsync();
-      for (int fi = warp - grp * GW; fi < nf; fi += GW) {
-        double acc = 0.0;
-        for (int q = lane; q < N2; q += 32) acc += sX[fi * N2 + q];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) a.facedot[f0 + fi] = acc;
-      }
-    }
     gsync();  // the stage and the tile are reused
+  }
+  if (POST && CG) {  // <p, w> of the plain operator -> alpha
+    double dummy = 0.0;
+    block_sum2(rz, dummy);
+    if (publish_last(a.part, rz, 0.0, &a.st->cnt[6])) {
+      double tot, t0;
+      final_sum2(a.part, gridDim.x, tot, t0);
+      if (threadIdx.x == 0) cg_set_alpha(a.st, tot);
+    }
   }
   if (RED) {
     double dummy = 0.0;
@@ -429,31 +428,6 @@ __global__ void __launch_bounds__(FxCfg<N, FK>::NT, (FxCfg<N, FK>::MINB)) fx_ker
 
 // ================================================================ CG helpers
 // <p, w> from the per-face dots of the operator kernel -> alpha (solver.py:303-310)
-__global__ void __launch_bounds__(HDGB_NT) reduce_pw_kernel(const double* __restrict__ facedot, int64_t nf,
-                                                            double* part, CGState* st) {
-  pdl_trigger();
-  pdl_wait();
-  if (st->done) return;
-  double s = 0.0, dummy = 0.0;
-  const int64_t per = (nf + gridDim.x - 1) / gridDim.x;
-  const int64_t b0 = blockIdx.x * per, b1 = min(nf, b0 + per);
-  for (int64_t q = b0 + threadIdx.x; q < b1; q += blockDim.x) s += facedot[q];
-  block_sum2(s, dummy);
-  if (publish_last(part, s, 0.0, &st->cnt[2])) {
-    double pw, z;
-    final_sum2(part, gridDim.x, pw, z);
-    if (threadIdx.x == 0) {
-      st->pw = pw;
-      if (!isfinite(pw) || pw <= 0.0) {
-        st->status = HDGB_EBREAKDOWN;
-        st->done = 1;
-      } else {
-        st->alpha = st->rho / pw;
-      }
-    }
-  }
-}
-
 // p = z + beta p (solver.py:320); also drives the device-side while loop of the PCG graph
 __global__ void p_update_kernel(const double* __restrict__ z, double* __restrict__ p, int64_t n, const CGState* st,
                                 cudaGraphConditionalHandle loop, int has_loop) {
@@ -808,7 +782,6 @@ cudaError_t launch_plain_post(hdgb_ctx* c, int cg, const double* u, double* r, c
   FaceArgs a = base_args(c, HDGB_PREC_NONE);
   a.in = u;
   a.out = r;
-  a.facedot = c->d_facedot;
   TabOff to;
   to.set(c->N);
   const double* MS = c->h_tab.data() + to.MS;
@@ -926,14 +899,6 @@ cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s) {
   a.w = v + V_W * c->vstride;
   a.out = v + V_Z * c->vstride;
   return face_any(c, OP_CG_UPDATE, kind, a, s);
-}
-
-cudaError_t launch_reduce_pw(hdgb_ctx* c, cudaStream_t s) {
-  int grid = (int)min((int64_t)HDGB_RED_BLOCKS, max((int64_t)1, c->nfaces / 64));
-  cudaError_t le = launch_pdl(reduce_pw_kernel, dim3(grid), dim3(HDGB_NT), 0, s, (const double*)c->d_facedot,
-                              c->nfaces, c->d_part, c->d_st);
-  c->launches++;
-  return le;
 }
 
 cudaError_t launch_p_update(hdgb_ctx* c, cudaStream_t s, cudaGraphConditionalHandle loop, int has_loop) {

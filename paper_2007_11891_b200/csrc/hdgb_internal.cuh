@@ -93,22 +93,35 @@ struct TabOff {
 // PCG device state (solver.py:282-321 scalars), lives in device memory.
 struct CGState {
   double rho, alpha, beta, norm0, thr, rn, pw, rr, rz, relres, rtol, atol;
+  double pw0;       // colour-0 part of <p, w> (transformed operator)
   int32_t it, max_iters, done, status, converged, pad;
-  uint32_t cnt[4];  // last-CTA tickets of the reduction kernels
+  uint32_t cnt[8];  // last-CTA tickets of the reduction kernels
 };
+
+// <p, w> complete -> alpha = rho / <p, w>, or breakdown (solver.py:305-310); thread 0 of the
+// last CTA of the kernel that finishes the operator
+__device__ __forceinline__ void cg_set_alpha(CGState* st, double pw) {
+  st->pw = pw;
+  if (!isfinite(pw) || pw <= 0.0) {
+    st->status = HDGB_EBREAKDOWN;
+    st->done = 1;
+  } else {
+    st->alpha = st->rho / pw;
+  }
+}
 
 struct OpArgs {
   Geo g;
   const double* u;
   double* r;
-  double* facedot;
   const double* tab;
   const double* dz;      // N^3 shared table (uniform) or nullptr
   const double* widths;  // n1+n2+n3 per-axis widths
   double lam;
   double al_u[4];        // uniform alpha0..alpha3
   int uniform;
-  const CGState* st;     // CG mode: early-exit flag
+  CGState* st;           // CG mode: early-exit flag, <p, w>
+  double* part;          // CG mode: per-CTA partials of <p, w>
 };
 
 struct FaceArgs {
@@ -130,7 +143,6 @@ struct FaceArgs {
   const double* w;
   double* z;
   double* part;          // per-CTA partials [gridDim][2]
-  double* facedot;       // per-face <u, r> (plain epilogue, CG mode)
   CGState* st;
 };
 
@@ -256,7 +268,6 @@ struct hdgb_ctx {
   double* d_y_full = nullptr;
   double* d_dn_full = nullptr;
   uint8_t* d_finfo = nullptr;     // per-face kind/class byte
-  double* d_facedot = nullptr;
   double* d_part = nullptr;
   std::vector<double> h_tab;      // host copy of d_tab (1D matrices become kernel parameters)
   std::vector<double> h_elem;     // pre/post tables D (n*n), B (n*2), C (n*2), tau_hat; empty until set

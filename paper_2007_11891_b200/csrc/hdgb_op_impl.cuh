@@ -29,7 +29,8 @@
 //   phase 2  thread q = (a1, a3) reduces U over a2 (y faces), thread q = (a1, a2) over a3
 //            (z faces);
 //   emit     contribution alpha_d GCC_ll u - g for the six faces at q (plus the colour-0
-//            partial, prefetched at the start of the element, in pass 1).
+//            partial, prefetched at the start of the element, in pass 1); CG mode zeroes
+//            the Dirichlet rows and accumulates <p, w> in registers, reduced once per kernel.
 //
 // Faces are staged with cp.async one element group ahead (double buffer).  The per-element
 // geometry (face ids, shared-face bits, kinds, metric terms) is computed once per element by
@@ -110,7 +111,7 @@ struct OpVCfg {
 #endif
   static constexpr int FS = 6 * NQ;                     // staged faces of one element
   static constexpr int VS = N * NQ;                     // U volume of one element
-  __host__ __device__ static constexpr int smem_doubles(bool cg) { return G * (2 * FS + VS + (cg ? FS : 0)); }
+  __host__ __device__ static constexpr int smem_doubles() { return G * (2 * FS + VS); }
 };
 
 // 1D reference-element tables as kernel parameters (constant bank): every compile-time
@@ -130,7 +131,7 @@ struct ElemInfo {
   int kind[6];
 };
 
-// MODE bit 0: CG (Dirichlet rows -> 0, per-face <u, r>); bit 1: non-uniform grid (per-element
+// MODE bit 0: CG (Dirichlet rows -> 0, <p, w> and alpha from a fixed-order reduction at the end); bit 1: non-uniform grid (per-element
 // metric terms and dz_inv); bit 2: "g only" (plain core: emit the eigen-space sum of g only).
 template <int N, int MODE, int COLOR>
 __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(const OpArgs a, int64_t t0, int64_t t1,
@@ -146,7 +147,6 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
   extern __shared__ __align__(16) double smem[];
   double* sF0 = smem;              // 2 x G x [6][NQ] staged faces
   double* sU = smem + 2 * G * FS;  // G x [N][NQ] volume
-  double* sDot = sU + G * VS;      // CG: G x [6][NQ] products u * r
   __shared__ ElemInfo sInfo[2][G];
   const Geo& g = a.g;
   const int tid = threadIdx.x;
@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
     }
   };
 
+  double dacc = 0.0;  // CG: this thread's share of <p, w> (fixed grid -> reproducible)
   int64_t gi = blockIdx.x;
   if (gi < ngroups) info(gi, sInfo[0]);
   __syncthreads();
@@ -224,7 +225,6 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
     const double al0 = I.al[0], al1 = I.al[1], al2 = I.al[2], al3 = I.al[3];
     const double* sF = sF0 + buf * G * FS + (act ? e : 0) * FS;
     double* vU = sU + (act ? e : 0) * VS;
-    double* dotp = sDot + (act ? e : 0) * FS;
     // colour-0 partials of the shared faces at q: issued now, consumed at the emits
     double prev[6];
     if (COLOR == 1 && on) {
@@ -237,10 +237,9 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
       const bool sh = shared >> s & 1u;
       double val = GONLY ? gval : ((s & 1) ? gcc1 : gcc0) * ua - gval;
       if (COLOR == 1 && sh) val = prev[s] + val;
-      const bool fin = COLOR == 1 || !sh;
-      if (CG) {
-        if (fin && kinds[s] == HDGB_DIRICHLET) val = 0.0;
-        dotp[s * NQ + q] = (fin && kind_counts(kinds[s])) ? ur * val : 0.0;
+      if (CG && (COLOR == 1 || !sh)) {  // final value of w here: Dirichlet row -> 0, <p, w>
+        if (kinds[s] == HDGB_DIRICHLET) val = 0.0;
+        if (kind_counts(kinds[s])) dacc = fma(ur, val, dacc);
       }
       a.r[off[s]] = val;
     };
@@ -288,29 +287,27 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
       emit(4, al3 * az0, al3 * zr0, zr0);
       emit(5, al3 * az1, al3 * zr1, zr1);
     }
-    if (CG) {  // per-face <u, r> of the final faces, fixed order
-      __syncthreads();
-      const int lane = tid & 31, warp = tid >> 5, nw = C::NT >> 5;
-      for (int f = warp; f < 6 * G; f += nw) {
-        const int fe = f / 6, s = f - (f / 6) * 6;
-        const ElemInfo& J = sInfo[buf][fe];
-        if (!J.valid || (COLOR == 0 && (J.shared >> s & 1u))) continue;
-        double acc = 0.0;
-        for (int k = lane; k < NQ; k += 32) acc += sDot[fe * FS + s * NQ + k];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) a.facedot[J.fid[s]] = acc;
-      }
-    }
     __syncthreads();  // staging buffer, volume and element info are reused
   }
   cp_async_wait_all();
+  if (CG && !GONLY) {  // <p, w>: colour 0 keeps its part, colour 1 completes it and sets alpha
+    double dummy = 0.0;
+    block_sum2(dacc, dummy);
+    if (publish_last(a.part, dacc, 0.0, &a.st->cnt[4 + COLOR])) {
+      double tot, t2;
+      final_sum2(a.part, gridDim.x, tot, t2);
+      if (threadIdx.x == 0) {
+        if (COLOR == 0) a.st->pw0 = tot;
+        else cg_set_alpha(a.st, a.st->pw0 + tot);
+      }
+    }
+  }
 }
 
 template <int N, int MODE, int COLOR>
 static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_t t1, cudaStream_t s) {
   using Cf = OpVCfg<N>;
-  const size_t smem = sizeof(double) * (size_t)Cf::smem_doubles(MODE & 1);
+  const size_t smem = sizeof(double) * (size_t)Cf::smem_doubles();
   auto kern = opV_kernel<N, MODE, COLOR>;
   static int cache[16] = {0};
   int64_t grid = 0;
@@ -356,7 +353,6 @@ static cudaError_t launch_t(hdgb_ctx* c, const double* u, double* r, cudaStream_
     if (e != cudaSuccess) return e;
     a.u = c->d_hat;
   }
-  a.facedot = c->d_facedot;
   a.tab = c->d_tab;
   a.dz = c->d_dz;
   a.widths = c->d_widths;
@@ -364,6 +360,7 @@ static cudaError_t launch_t(hdgb_ctx* c, const double* u, double* r, cudaStream_
   for (int q = 0; q < 4; ++q) a.al_u[q] = c->al_u[q];
   a.uniform = c->uniform;
   a.st = c->d_st;
+  a.part = c->d_part;
   // z-slabs of element pairs, sized so two slabs of face data stay L2-resident
   const int64_t hp = (g.n1 + 1) / 2;
   const int64_t per_k = hp * g.n2;  // pairs per z-layer
