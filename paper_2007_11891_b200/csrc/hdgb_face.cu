@@ -175,7 +175,10 @@ struct FxCfg {
 #else
   // measured (config-3 sweep): capping registers for more resident CTAs raises DRAM traffic
   // (L2 thrashing between the staged reads and the write-back) more than it hides latency
-  static constexpr int MINB = 2;
+#ifndef HDGB_FX_MINB_POST
+#define HDGB_FX_MINB_POST 2
+#endif
+  static constexpr int MINB = FK == FX_POST ? HDGB_FX_MINB_POST : 2;
 #endif
 };
 
