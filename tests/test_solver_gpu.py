@@ -178,3 +178,27 @@ def test_device_hybridize_matches_host(uniform):
     unk = np.concatenate([np.repeat(mesh.face_kind[d] != hb.DIRICHLET, (p + 1) ** 2) for d in range(3)])
     assert np.max(np.abs(dv[unk] - hv[unk])) <= 1e-12 * np.max(np.abs(hv))
     assert np.all(dv[~unk] == 0.0)
+
+
+def test_device_resident_solve_with_neumann_data_matches_host_pipeline():
+    """Mixed Dirichlet/Neumann boundary data through the device-resident solve."""
+    bc = ("neumann", "dirichlet", "dirichlet", "neumann", "dirichlet", "dirichlet")
+    mesh = hb.Mesh((3, 2, 2), (0.0, 0.0, 0.0), (TWO_PI, 2 * TWO_PI / 3, 2 * TWO_PI / 3), bc)
+    cfg = hb.SolverConfig(lam=0.3, preconditioner="block")
+    ctx = hb.make_context(mesh, 4, cfg)
+    b = ctx.basis
+    f = _field(mesh, b, lambda a, bb, c: (0.3 + 3.0) * smooth_u(a, bb, c))
+    g_D = _dirichlet(mesh, b, smooth_u)
+    g_N = hb.FluxField(mesh, b.p)
+    rng = np.random.default_rng(12)
+    for d in range(3):
+        m = mesh.face_kind[d] == hb.NEUMANN
+        g_N.data[d][m] = rng.uniform(-0.5, 0.5, g_N.data[d][m].shape)
+    u0 = np.zeros((mesh.n_elements,) + (b.n,) * 3)
+    u_d, q_d, rd = hb.solve(u0, f, g_D, g_N, cfg, ctx)
+    ctx_h = hb.make_context(mesh, 4, cfg, counter=hb.FlopCounter())
+    u_h, q_h, rh = hb.solve(u0, f, g_D, g_N, cfg, ctx_h)
+    assert rd.converged and abs(rd.iterations - rh.iterations) <= 1
+    assert np.max(np.abs(u_d - u_h)) <= 1e-8 * np.max(np.abs(u_h))
+    for d in range(3):
+        assert np.max(np.abs(q_d[d] - q_h[d])) <= 1e-8 * np.max(np.abs(q_h[d]))
