@@ -111,7 +111,15 @@ struct OpVCfg {
 #endif
   static constexpr int FS = 6 * NQ;                     // staged faces of one element
   static constexpr int VS = N * NQ;                     // U volume of one element
-  __host__ __device__ static constexpr int smem_doubles() { return G * (2 * FS + VS); }
+  // dz_inv lines in registers (N values per thread) up to N = 11; from a shared copy of the
+  // table for N >= 12, where the registers are worth more (measured: p = 12 339 -> 312 us,
+  // p = 16 490 -> 433 us; slower below)
+#ifdef HDGB_OPV_DZSMEM
+  static constexpr bool DZS = HDGB_OPV_DZSMEM;
+#else
+  static constexpr bool DZS = N >= 12;
+#endif
+  __host__ __device__ static constexpr int smem_doubles() { return G * (2 * FS + VS) + (DZS ? N * NQ : 0); }
 };
 
 // 1D reference-element tables as kernel parameters (constant bank): every compile-time
@@ -160,10 +168,14 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
   const double b0a = a.tab[to.BS + 2 * qa], b1a = a.tab[to.BS + 2 * qa + 1];
   const double b0b = a.tab[to.BS + 2 * qb], b1b = a.tab[to.BS + 2 * qb + 1];
   const double lama = a.tab[to.Lam + qa], lamb = a.tab[to.Lam + qb];
-  double dzr[UNI ? N : 1];
-  if (UNI) {
+  constexpr bool DZR = UNI && !C::DZS;
+  double dzr[DZR ? N : 1];
+  double* sDz = smem + G * (2 * FS + VS);
+  if (DZR) {
 #pragma unroll
-    for (int a1 = 0; a1 < N; ++a1) dzr[UNI ? a1 : 0] = __ldg(a.dz + a1 * NQ + q);  // dz_inv[a1][a2][a3]
+    for (int a1 = 0; a1 < N; ++a1) dzr[DZR ? a1 : 0] = __ldg(a.dz + a1 * NQ + q);  // dz_inv[a1][a2][a3]
+  } else if (UNI) {
+    for (int i = tid; i < N * NQ; i += blockDim.x) sDz[i] = __ldg(a.dz + i);
   }
 
   const int64_t ngroups = (t1 - t0 + G - 1) / G;
@@ -259,7 +271,8 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
         F = fma(by1, y1, F);
         F = fma(bz0, z0, F);
         F = fma(bz1, z1, F);
-        const double dzv = UNI ? dzr[UNI ? a1 : 0] : __drcp_rn(fma(al1, K.Lam[a1], base));  // EigenScale3D
+        const double dzv = DZR ? dzr[DZR ? a1 : 0]
+                               : (UNI ? sDz[a1 * NQ + q] : __drcp_rn(fma(al1, K.Lam[a1], base)));  // EigenScale3D
         const double U = F * dzv;
         vU[a1 * NQ + q] = U;
         ax0 = fma(K.B0[a1], U, ax0);
