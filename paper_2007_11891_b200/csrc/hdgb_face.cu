@@ -165,9 +165,16 @@ struct FxCfg {
   static constexpr int S = N <= 11 ? 3 : 2;          // ring stages per group
 #endif
   static constexpr int EPT = (FPW * N2 + GT - 1) / GT;  // epilogue values per thread
+  // FX_POST stages u next to G with the same bulk copies for N <= 11 (measured: p = 8 plain
+  // 446 -> 420 us with 3 CTAs/SM); larger N prefetch u into registers (p = 12/16 faster)
+#ifdef HDGB_FX_POST_TMA
+  static constexpr int OPS = (FK == FX_POST && HDGB_FX_POST_TMA) ? 2 : 1;
+#else
+  static constexpr int OPS = (FK == FX_POST && N <= 11) ? 2 : 1;
+#endif
   static constexpr bool BLOCK = FK == FX_PREC || FK == FX_INIT || FK == FX_UPDATE;
   // per-group slice, 128-byte aligned (bulk-copy destinations need 16)
-  __host__ __device__ static constexpr int per_group() { return (S * BATW + FPW * WP + 15) / 16 * 16; }
+  __host__ __device__ static constexpr int per_group() { return (S * OPS * BATW + FPW * WP + 15) / 16 * 16; }
   static constexpr int YT = BLOCK ? 9 * N2 : 0;      // uniform-grid y^-1 class tables
   static constexpr int smem_doubles() { return NG * per_group() + (YT + 1) / 2 * 2; }
 #ifdef HDGB_FX_MINB
@@ -175,10 +182,11 @@ struct FxCfg {
 #else
   // measured (config-3 sweep): capping registers for more resident CTAs raises DRAM traffic
   // (L2 thrashing between the staged reads and the write-back) more than it hides latency
-#ifndef HDGB_FX_MINB_POST
-#define HDGB_FX_MINB_POST 2
-#endif
+#ifdef HDGB_FX_MINB_POST
   static constexpr int MINB = FK == FX_POST ? HDGB_FX_MINB_POST : 2;
+#else
+  static constexpr int MINB = (FK == FX_POST && OPS == 2) ? 3 : 2;
+#endif
 #endif
 };
 
@@ -239,7 +247,8 @@ __global__ void __launch_bounds__(FxCfg<N, FK>::NT, (FxCfg<N, FK>::MINB)) fx_ker
                                                                      const __grid_constant__ FxMats<N> M) {
   using C = FxCfg<N, FK>;
   constexpr int N2 = C::N2, FPW = C::FPW, NP = C::NP, WP = C::WP, BATW = C::BATW, S = C::S, GT = C::GT;
-  constexpr int GW = C::GW, EPT = C::EPT;
+  constexpr int GW = C::GW, EPT = C::EPT, OPS = C::OPS;
+  constexpr bool UTMA = OPS == 2;
   constexpr bool BLOCK = C::BLOCK;
   constexpr bool RED = FK == FX_INIT || FK == FX_UPDATE;
   constexpr bool POST = FK == FX_POST;
@@ -256,8 +265,8 @@ __global__ void __launch_bounds__(FxCfg<N, FK>::NT, (FxCfg<N, FK>::MINB)) fx_ker
   const int grp = warp / GW, gl = threadIdx.x - grp * GT;  // group and thread within it
   const int f = gl / N, l = gl - (gl / N) * N;
   const bool on_lane = f < FPW;
-  double* sStage = smem + grp * C::per_group();  // S x BATW
-  double* sW = sStage + S * BATW;                // FPW x WP exchange tile
+  double* sStage = smem + grp * C::per_group();  // S x OPS x BATW
+  double* sW = sStage + S * OPS * BATW;          // FPW x WP exchange tile
   double* sY = smem + C::NG * C::per_group();    // y^-1 class tables (uniform grids)
   if (POST && threadIdx.x < N) sWq[threadIdx.x] = M.B[threadIdx.x];
   if (BLOCK && a.ycls)
@@ -287,11 +296,15 @@ __global__ void __launch_bounds__(FxCfg<N, FK>::NT, (FxCfg<N, FK>::MINB)) fx_ker
     const int nf = (int)min((int64_t)FPW, a.nfaces - f0);
     const int64_t s0 = f0 * N2, lo = s0 & ~(int64_t)1;
     const uint32_t total = (uint32_t)(s0 - lo) + (uint32_t)nf * N2, bulk = total & ~1u;
-    double* dst = sStage + (k % S) * BATW;
+    double* dst = sStage + (k % S) * OPS * BATW;
     uint64_t* bar = &sBar[grp][k % S];
-    if (bulk != total) dst[bulk] = src[lo + bulk];
-    mbar_expect_tx(bar, bulk * 8u);
+    if (bulk != total) {
+      dst[bulk] = src[lo + bulk];
+      if (UTMA) dst[BATW + bulk] = a.in[lo + bulk];
+    }
+    mbar_expect_tx(bar, bulk * 8u * OPS);
     bulk_g2s(dst, src + lo, bulk * 8u, bar);
+    if (UTMA) bulk_g2s(dst + BATW, a.in + lo, bulk * 8u, bar);
   };
   if (gl == 0)
     for (int64_t k = 0; k < S - 1 && k < nmine; ++k) issue(k);
@@ -305,14 +318,14 @@ __global__ void __launch_bounds__(FxCfg<N, FK>::NT, (FxCfg<N, FK>::MINB)) fx_ker
     const int nf = (int)min((int64_t)FPW, a.nfaces - f0);
     const int nv = nf * N2;
     const bool on = on_lane && f < nf;
-    double* sX = sStage + (k % S) * BATW + (int)((f0 * N2) & 1);  // face fi at sX + fi * N2
+    double* sX = sStage + (k % S) * OPS * BATW + (int)((f0 * N2) & 1);  // face fi at sX + fi * N2 (u at + BATW)
     const uint8_t inf = on ? finfo[f0 + f] : 0;
-    double uv[POST ? EPT : 1];
-    if (POST) {  // u for the epilogue, in flight during the passes (coalesced)
+    double uv[(POST && !UTMA) ? EPT : 1];
+    if (POST && !UTMA) {  // u for the epilogue, in flight during the passes (coalesced)
 #pragma unroll
       for (int m = 0; m < EPT; ++m) {
         const int it = gl + m * GT;
-        if (it < nv) uv[POST ? m : 0] = a.in[f0 * N2 + it];
+        if (it < nv) uv[(POST && !UTMA) ? m : 0] = a.in[f0 * N2 + it];
       }
     }
     mbar_wait(&sBar[grp][k % S], (uint32_t)(k / S) & 1u);
@@ -393,7 +406,7 @@ __global__ void __launch_bounds__(FxCfg<N, FK>::NT, (FxCfg<N, FK>::MINB)) fx_ker
       double v = ODD ? sX[it] : sW[fi * WP + j * NP + kk];
       if (POST) {
         // r = (sum_sides alpha_d GCC_ll) (w (x) w) u - (MS (x) MS) G
-        const double u0 = uv[POST ? m : 0];
+        const double u0 = UTMA ? sX[BATW + it] : uv[(POST && !UTMA) ? m : 0];
         v = ((__ldg(fcoef + f0 + fi) * sWq[j]) * sWq[kk]) * u0 - v;
         if (CG) {  // final w: Dirichlet row -> 0, <p, w> (p = u here)
           const int kind = finfo_kind(__ldg(finfo + f0 + fi));
