@@ -185,7 +185,9 @@ struct FxCfg {
 #ifdef HDGB_FX_MINB_POST
   static constexpr int MINB = FK == FX_POST ? HDGB_FX_MINB_POST : 2;
 #else
-  static constexpr int MINB = (FK == FX_POST && OPS == 2) ? 3 : 2;
+  // (measured) 3 CTAs/SM for the block preconditioner (p = 8: 130 -> 116 us) and the staged
+  // plain epilogue; 2 for the plain pre-transform
+  static constexpr int MINB = ((FK == FX_POST && OPS == 2) || (BLOCK && N >= 8)) ? 3 : 2;
 #endif
 #endif
 };
