@@ -280,9 +280,7 @@ struct hdgb_ctx {
   cudaStream_t s = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaGraphExec_t graph[2][4] = {{nullptr}};
-  int graph_iters = 0;
   int64_t launches = 0;
-  int smem_op = 0;
   // L2 working-set target of one z-slab of the colour passes; 0 = one slab.  Slabbing cuts
   // HBM traffic (pass-0 partials stay in L2) but multiplies launches; while the element
   // kernels are issue-bound the single slab is faster (HDGB_SLAB_MB overrides).
@@ -306,7 +304,6 @@ cudaError_t launch_cg_init(hdgb_ctx* c, int kind, cudaStream_t s);
 cudaError_t launch_diag_user(hdgb_ctx* c, const double* diag, const double* in, double* out, cudaStream_t s);
 int grid_for(int64_t work, int per);
 cudaError_t launch_build_tables(hdgb_ctx* c, cudaStream_t s);
-cudaError_t op_set_smem_limits(hdgb_ctx* c);
 }  // namespace hdgb
 
 namespace hdgb {
