@@ -331,3 +331,29 @@ def test_face_dot_counts_unknown_faces_once():
     dc.face_dot(_dev(a), _dev(b), out)
     pa, pb = hb.pack_unknowns(hb.unpack_all(a, mesh, ctx.basis.p)), hb.pack_unknowns(hb.unpack_all(b, mesh, ctx.basis.p))
     assert abs(float(out.item()) - float(np.dot(pa, pb))) <= 1e-12 * np.abs(pa * pb).sum()
+
+
+@pytest.mark.parametrize("n_el,p", [((1, 1, 1), 3), ((1, 2, 3), 2), ((5, 1, 2), 6), ((2, 3, 1), 9)])
+def test_small_and_flat_grids_match_oracle(n_el, p):
+    """Degenerate grids: a single element, single-element layers, odd/even pair counts."""
+    bc = ("dirichlet", "neumann", "neumann", "dirichlet", "neumann", "dirichlet")
+    hi = tuple(0.5 * v for v in n_el)
+    mesh = hb.Mesh(n_el, (0, 0, 0), hi, bc)
+    ctx = hb.OperatorContext(hb.Basis1D(p, 0.6), mesh, 0.9)
+    octx = O.context(O.basis_1d(p, 0.6), O.Grid.uniform(n_el, (0, 0, 0), hi, bc), 0.9)
+    u = np.random.default_rng(sum(n_el) + p).uniform(-1, 1, mesh.n_all(p))
+    dc = hb.device_context(ctx)
+    for variant, tr in ((0, False), (1, True)):
+        assert relerr(dc.apply(_dev(u), variant).cpu().numpy(), O.apply_op(octx, u, tr)) < TOL
+    y = O.face_selfcoupling(octx)
+    assert relerr(dc.prec(_dev(u), 1).cpu().numpy(), O.block_prec_apply(octx, y, u)) < TOL
+    F = np.random.default_rng(p).uniform(-1, 1, mesh.n_trace_unknowns(p))
+    x, it, rel, conv = hb.pcg(hb.DeviceOperator(ctx, 1), hb.transformed_preconditioner(ctx).apply_packed, F,
+                              np.zeros_like(F), rtol=1e-10)
+    grid, n = octx["grid"], octx["n"]
+    ydiag = O.eigen_diagonal(octx)
+    xo, ito, _, _ = O.pcg(lambda v: O.apply_op_packed(octx, v, True),
+                          lambda r: O.pack(grid, n, O.diag_prec_apply(grid, n, ydiag, O.unpack(grid, n, r))),
+                          F, np.zeros_like(F))
+    assert conv and abs(it - ito) <= 1, (it, ito)
+    assert relerr(x, xo) < 1e-9
