@@ -137,7 +137,8 @@ __global__ void __launch_bounds__(256) pw_kernel(FaceArgs a, const uint8_t* __re
 //  * the 1D matrices are kernel parameters (constant bank): each line pass is N independent
 //    DFMA chains with uniform operands;
 //  * results leave through coalesced stores; the uniform-grid y^-1 class tables sit in
-//    shared memory.
+//    shared memory; the plain epilogue (FX_POST) stages u next to G for N <= 11 and finishes
+//    <p, w> and alpha in CG mode (one fixed-order reduction per kernel).
 enum { FX_TRANSFORM = 0, FX_POST = 1, FX_PREC = 2, FX_INIT = 3, FX_UPDATE = 4 };
 
 template <int N, int FK>
@@ -177,18 +178,14 @@ struct FxCfg {
   __host__ __device__ static constexpr int per_group() { return (S * OPS * BATW + FPW * WP + 15) / 16 * 16; }
   static constexpr int YT = BLOCK ? 9 * N2 : 0;      // uniform-grid y^-1 class tables
   static constexpr int smem_doubles() { return NG * per_group() + (YT + 1) / 2 * 2; }
+  // register budget (resident CTAs per SM), measured on the config-3 sweep: 3 for the block
+  // preconditioner at N >= 8 (p = 8: 130 -> 116 us) and for the staged plain epilogue; 2 for the
+  // plain pre-transform, where more resident CTAs raised DRAM traffic (L2 thrashing between
+  // the staged reads and the write-back) more than they hid latency.  HDGB_FX_MINB overrides.
 #ifdef HDGB_FX_MINB
   static constexpr int MINB = HDGB_FX_MINB;
 #else
-  // measured (config-3 sweep): capping registers for more resident CTAs raises DRAM traffic
-  // (L2 thrashing between the staged reads and the write-back) more than it hides latency
-#ifdef HDGB_FX_MINB_POST
-  static constexpr int MINB = FK == FX_POST ? HDGB_FX_MINB_POST : 2;
-#else
-  // (measured) 3 CTAs/SM for the block preconditioner (p = 8: 130 -> 116 us) and the staged
-  // plain epilogue; 2 for the plain pre-transform
   static constexpr int MINB = ((FK == FX_POST && OPS == 2) || (BLOCK && N >= 8)) ? 3 : 2;
-#endif
 #endif
 };
 
