@@ -13,10 +13,10 @@ Dirichlet lift, hybridised initial guess, interior recovery;
 solver.py:129-279; SURVEY §8f "next" #1): `solve` / `solve_transformed`
 run the element RHS and the interior recovery on the device
 (csrc/hdgb_elem.cu) and keep every vector device-resident from the RHS to
-(u, q); the host restatements below (generalised to per-element geometry
-for non-uniform grids) remain the public pre/post functions, the parity
-reference of the device versions, and the path taken when a FlopCounter
-is attached (it counts per host call).
+(u, q), with the reference's FlopCounter totals added analytically; the host
+restatements below (generalised to per-element geometry for non-uniform
+grids) remain the public pre/post functions and the parity reference of the
+device versions (`solve_host_pipeline`).
 """
 
 import math
@@ -41,7 +41,7 @@ from .preconditioner import (
 
 __all__ = ["SolverConfig", "SolveReport", "make_context", "resolve_tau_hat", "apply_element_inverse",
            "hybridize_initial_guess", "build_rhs", "recover_interior", "pcg", "solve", "solve_transformed",
-           "DeviceOperator"]
+           "solve_host_pipeline", "solve_transformed_host_pipeline", "solve_flop_count", "DeviceOperator"]
 
 PRECONDITIONER_KINDS = ("none", "diagonal", "block", "transformed")
 
@@ -494,6 +494,30 @@ def _ops(ctx):
 _PREC_KIND = {"none": _lib.PREC_NONE, "diagonal": _lib.PREC_DIAG_NODAL, "block": _lib.PREC_BLOCK}
 
 
+def solve_flop_count(mesh, p, iterations, transformed=False, dirichlet_lift=False):
+    """FlopCounter total of one reference solve (operator.py:47-68 semantics, solver.py:338-410).
+
+    The element inverse counts its nine axis contractions (2 n per volume point each) plus the
+    dz_inv scaling; build_rhs and recover_interior each add one inverse and their face
+    couplings (24 per volume point); pcg applies K once for the initial residual and once per
+    iteration (n_e (73 | 25) n^3 + 12 n^2 each; its preconditioner applies are not counted);
+    the Dirichlet lift is one more K apply; the transformed solve adds three face transforms
+    (4 n^3 per face each).
+    """
+    n = p + 1
+    ne = mesh.n_elements
+    V = ne * n ** 3
+    inv = 24 * n * V + V
+    op_plain = ne * (73 * n ** 3 + 12 * n ** 2)
+    op = ne * ((25 if transformed else 73) * n ** 3 + 12 * n ** 2)
+    total = 2 * (inv + 24 * V) + (iterations + 1) * op
+    if dirichlet_lift:
+        total += op_plain
+    if transformed:
+        total += 3 * 4 * n ** 3 * sum(mesh.n_faces)
+    return total
+
+
 def _solve_device(u0, f, g_D, g_N, cfg, ctx, transformed):
     """Device-resident solve: element RHS, fused PCG and interior recovery on the GPU.
 
@@ -505,6 +529,7 @@ def _solve_device(u0, f, g_D, g_N, cfg, ctx, transformed):
     dc = device_context(ctx)
     mesh, p = ctx.mesh, ctx.basis.p
     dev = f"cuda:{dc.device}"
+    counter = getattr(ctx, "counter", None)
     F = dc.build_rhs(f)
     if g_N is not None:  # Neumann data (solver.py:233-237)
         neu = FluxField(mesh, p)
@@ -542,25 +567,32 @@ def _solve_device(u0, f, g_D, g_N, cfg, ctx, transformed):
     t0 = time.perf_counter()
     iters, relres, conv = dc.pcg(variant, kind, F, x, cfg.rtol, cfg.atol, cfg.max_iters)
     wall = time.perf_counter() - t0
+    flops = solve_flop_count(mesh, p, iters, transformed, lift is not None)
+    if counter is not None:
+        counter.ops += flops
     if transformed:
         x = dc.transform(x, np.ascontiguousarray(ctx.basis.S))
     if lift is not None:
         x += lift  # _restore_dirichlet: Dirichlet slots are zero after the solve
     u, qs = dc.recover_interior(f, x)
     return (u.cpu().numpy(), tuple(q.cpu().numpy() for q in qs),
-            SolveReport(iters, relres, conv, wall, wall / max(iters, 1), None))
+            SolveReport(iters, relres, conv, wall, wall / max(iters, 1), None if counter is None else flops))
 
 
 def solve(u0, f, g_D, g_N, cfg, ctx):
     """Hybridise, build the RHS, iterate on the device, recover (u, q) (solver.py:338-369).
 
-    Runs device-resident (`_solve_device`) unless the context carries a FlopCounter, whose
-    per-call accounting follows the host pipeline below.
+    Device-resident (`_solve_device`); `solve_host_pipeline` keeps the host pre/post path.
     """
     if cfg.preconditioner == "transformed":
         return solve_transformed(u0, f, g_D, g_N, cfg, ctx)
-    if getattr(ctx, "counter", None) is None:
-        return _solve_device(u0, f, g_D, g_N, cfg, ctx, False)
+    return _solve_device(u0, f, g_D, g_N, cfg, ctx, False)
+
+
+def solve_host_pipeline(u0, f, g_D, g_N, cfg, ctx):
+    """solve() with the host pre/post restatements around the device PCG (parity reference)."""
+    if cfg.preconditioner == "transformed":
+        return solve_transformed_host_pipeline(u0, f, g_D, g_N, cfg, ctx)
     ops0 = _ops(ctx)
     prec = _build_preconditioner(cfg.preconditioner, ctx)
     u_tilde0 = hybridize_initial_guess(u0, ctx, g_D, g_N)
@@ -582,8 +614,11 @@ def solve(u0, f, g_D, g_N, cfg, ctx):
 
 def solve_transformed(u0, f, g_D, g_N, cfg, ctx):
     """Same pipeline in the transformed basis (solver.py:372-410, Alg. 6)."""
-    if getattr(ctx, "counter", None) is None:
-        return _solve_device(u0, f, g_D, g_N, cfg, ctx, True)
+    return _solve_device(u0, f, g_D, g_N, cfg, ctx, True)
+
+
+def solve_transformed_host_pipeline(u0, f, g_D, g_N, cfg, ctx):
+    """solve_transformed() with the host pre/post restatements (parity reference)."""
     ops0 = _ops(ctx)
     prec = transformed_preconditioner(ctx)
     u_tilde0 = hybridize_initial_guess(u0, ctx, g_D, g_N)

@@ -97,3 +97,37 @@ def test_flop_counter_semantics():
     c.reset()
     assert c.ops == 0
     assert _lib.PLAIN == 0 and _lib.TRANSFORMED == 1
+
+
+def test_solve_flop_count_matches_reference_counter():
+    """solve_flop_count vs the reference's own FlopCounter over a full host solve (CPU)."""
+    import os
+    import sys
+
+    import numpy as np
+    import pytest
+
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference tree not present")
+    sys.path.insert(0, ref)
+    try:
+        import hdgbox as R
+    finally:
+        sys.path.remove(ref)
+    import paper_2007_11891_b200 as hb
+
+    for precond, p in (("block", 3), ("transformed", 2)):
+        mesh = R.Mesh((2, 2, 2), (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), "dirichlet")
+        cfg = R.SolverConfig(lam=0.5, preconditioner=precond, measure_ops=True)
+        ctx = R.make_context(mesh, p, cfg)
+        n = p + 1
+        X1, X2, X3 = mesh.element_node_grids(ctx.basis.nodes)
+        f = np.broadcast_to(np.sin(np.pi * X1) * np.sin(np.pi * X2) * np.sin(np.pi * X3),
+                            (mesh.n_elements,) + (n,) * 3).copy()
+        g_D = R.FluxField(mesh, p)
+        for d in range(3):
+            g_D.data[d][mesh.face_kind[d] == R.DIRICHLET] = 0.25
+        _, _, rep = R.solve(np.zeros_like(f), f, g_D, None, cfg, ctx)
+        mine = hb.Mesh((2, 2, 2), (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), "dirichlet")
+        assert rep.flops == hb.solve_flop_count(mine, p, rep.iterations, precond == "transformed", True)

@@ -137,12 +137,11 @@ def test_device_pre_post_nonuniform_grid():
 
 @pytest.mark.parametrize("precond", ["block", "transformed"])
 def test_device_resident_solve_matches_host_pipeline(precond):
-    """solve() device-resident path vs the host pre/post pipeline (FlopCounter attached)."""
+    """solve() device-resident path vs the host pre/post pipeline."""
     mesh, cfg, ctx, f, g_D, _ = make_problem(p=5, lam=0.5, precond=precond)
     u0 = np.random.default_rng(2).uniform(-1, 1, (mesh.n_elements,) + (ctx.basis.n,) * 3)
     u_d, q_d, rd = hb.solve(u0, f, g_D, None, cfg, ctx)
-    ctx_h = hb.make_context(mesh, 5, cfg, counter=hb.FlopCounter())
-    u_h, q_h, rh = hb.solve(u0, f, g_D, None, cfg, ctx_h)
+    u_h, q_h, rh = hb.solve_host_pipeline(u0, f, g_D, None, cfg, ctx)
     assert rd.converged and abs(rd.iterations - rh.iterations) <= 1
     assert np.max(np.abs(u_d - u_h)) <= 1e-8 * np.max(np.abs(u_h))
     for d in range(3):
@@ -196,9 +195,16 @@ def test_device_resident_solve_with_neumann_data_matches_host_pipeline():
         g_N.data[d][m] = rng.uniform(-0.5, 0.5, g_N.data[d][m].shape)
     u0 = np.zeros((mesh.n_elements,) + (b.n,) * 3)
     u_d, q_d, rd = hb.solve(u0, f, g_D, g_N, cfg, ctx)
-    ctx_h = hb.make_context(mesh, 4, cfg, counter=hb.FlopCounter())
-    u_h, q_h, rh = hb.solve(u0, f, g_D, g_N, cfg, ctx_h)
+    u_h, q_h, rh = hb.solve_host_pipeline(u0, f, g_D, g_N, cfg, ctx)
     assert rd.converged and abs(rd.iterations - rh.iterations) <= 1
     assert np.max(np.abs(u_d - u_h)) <= 1e-8 * np.max(np.abs(u_h))
     for d in range(3):
         assert np.max(np.abs(q_d[d] - q_h[d])) <= 1e-8 * np.max(np.abs(q_h[d]))
+
+
+def test_device_solve_reports_reference_flop_totals():
+    mesh, cfg, ctx, f, g_D, _ = make_problem(p=3, precond="block")
+    ctx_c = hb.make_context(mesh, 3, cfg, counter=hb.FlopCounter())
+    u0 = np.zeros((mesh.n_elements,) + (ctx.basis.n,) * 3)
+    _, _, rep = hb.solve(u0, f, g_D, None, cfg, ctx_c)
+    assert rep.flops == hb.solve_flop_count(mesh, 3, rep.iterations, False, True) == ctx_c.counter.ops
