@@ -9,7 +9,8 @@ uniform[-1,1] trace vector resident in HBM; the 8.5 MB vectors fit in L2, so
 L2 is flushed (a 512 MB write) before every timed step and only the apply is
 inside the CUDA events.  `value` = trace unknowns / apply time (trace-DOF/s).
 `e2e` times the same apply through the C ABI with pinned HOST buffers
-(hdgb_op_apply_host: H2D + kernel + D2H).  The line also carries the fused
+(hdgb_op_apply_host_packed: H2D + kernels + D2H on packed unknown vectors, the
+reference's apply_K closure).  The line also carries the fused
 block-PCG solve of the same config (CG us per unknown per iteration), the
 transformed (Alg. 3) apply, the roofline of the operator kernel, and the CPU
 oracle timed on this host.
@@ -234,6 +235,30 @@ def _large_point(hb, p, m, lam, flush, stream, hbm, fp64_peak, reps=10):
         if name == "transformed":
             ent["fp64_frac"] = mesh.n_elements * (25 * n ** 3 + 12 * n ** 2) / t / 1e12 / fp64_peak
         out[name] = ent
+    # PCG iteration cost: F = the seeded vector, x0 = 0, 10 fixed
+    # iterations (rtol tiny), fused device PCG; block (Alg. 2 + Alg. 4) and transformed pipelines
+    F = r.clone()
+    F.copy_(u)
+    dc.zero_dirichlet(F)
+    x = torch.zeros_like(F)
+    iters = 10
+    for name, variant, kind in (("pcg_block", 0, 1), ("pcg_transformed", 1, 3)):
+        x.zero_()
+        dc.pcg(variant, kind, F, x, 1e-300, 0.0, iters)
+        ts = []
+        for _ in range(3):
+            flush.zero_()
+            x.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            it, _, _ = dc.pcg(variant, kind, F, x, 1e-300, 0.0, iters)
+            b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b) * 1e-3)
+        t_it = statistics.median(ts) / max(it, 1)
+        out[name] = {"us_per_iter": t_it * 1e6, "ps_per_unknown_per_iter": t_it / N * 1e12,
+                     "hbm_frac_of_96B_per_unknown": 96 * N_all / t_it / 1e9 / hbm, "iterations": it}
     del dc, ctx, u, r
     torch.cuda.empty_cache()
     return out
@@ -366,14 +391,16 @@ def run_ours(args):
     achieved = alg_bytes / t_tr / 1e9
     traffic = _traffic_record()
 
-    # ---- e2e through the C ABI with pinned host buffers
-    h_u = torch.empty(N_all, dtype=torch.float64).pin_memory()
-    h_r = torch.empty(N_all, dtype=torch.float64).pin_memory()
-    h_u.copy_(u.cpu())
+    # ---- e2e through the C ABI with pinned host buffers: the reference's apply_K closure on
+    # packed unknown vectors (hdgb_op_apply_host_packed: H2D, unpack, apply, pack, D2H, sync)
+    n_e2e = dc.n_unknown if world == 1 else N_all
+    h_u = torch.empty(n_e2e, dtype=torch.float64).pin_memory()
+    h_r = torch.empty(n_e2e, dtype=torch.float64).pin_memory()
+    h_u.copy_(dc.pack(u).cpu() if world == 1 else u.cpu())
     hu, hr = h_u.numpy(), h_r.numpy()
     def e2e_step():
         if world == 1:
-            dc.apply_host(hu, hr, 0)  # C ABI: H2D + kernel + D2H + sync
+            dc.apply_host_packed(hu, hr, 0)
         else:
             ud = h_u.to("cuda", non_blocking=True)
             dc.apply(ud, 0, out=r)
@@ -396,7 +423,8 @@ def run_ours(args):
         e2e_ms.append(a.elapsed_time(b))
     t_e2e = statistics.median(e2e_ms) * 1e-3
     apply_step(0)
-    assert np.array_equal(hr, r.cpu().numpy()), "e2e result differs from the device-resident apply"
+    ref_e2e = dc.pack(r).cpu().numpy() if world == 1 else r.cpu().numpy()
+    assert np.array_equal(hr, ref_e2e), "e2e result differs from the device-resident apply"
 
     # ---- fused block-PCG solve (CG us per unknown per iteration)
     cg = None
@@ -546,9 +574,9 @@ def run_ours(args):
         "solve": solve_rec,
         "large": large,
         "cpu_baseline": cpu,
-        "e2e": {"value": world * N / t_e2e, "unit": "trace-DOF/s", "h2d_bytes_per_step": 8 * N_all,
-                "d2h_bytes_per_step": 8 * N_all, "ms_per_step": t_e2e * 1e3,
-                "path": "hdgb_op_apply_host (C ABI, pinned host buffers)"},
+        "e2e": {"value": world * N / t_e2e, "unit": "trace-DOF/s", "h2d_bytes_per_step": 8 * n_e2e,
+                "d2h_bytes_per_step": 8 * n_e2e, "ms_per_step": t_e2e * 1e3,
+                "path": "hdgb_op_apply_host_packed (C ABI, pinned host buffers, packed unknown vectors)"},
         "gpu_launches": launches,
         "clocks": clk.record(),
     }

@@ -85,6 +85,9 @@ int hdgb_op_apply(hdgb_ctx* ctx, int variant, const double* u, double* r, void* 
 /* Same with HOST buffers (pinned for full PCIe speed): copies in, applies, copies out,
  * synchronizes.  The e2e path of bench.py. */
 int hdgb_op_apply_host(hdgb_ctx* ctx, int variant, const double* u_host, double* r_host, void* stream);
+/* The reference's apply_K closure (solver.py:348-349): packed unknown vectors in and out
+ * (pack_unknowns order, mesh.py:318-351), HOST buffers; unpack, apply, pack on the device. */
+int hdgb_op_apply_host_packed(hdgb_ctx* ctx, int variant, const double* v_host, double* r_host, void* stream);
 
 /* out = (A (x) A) in on every face block (transform_faces, operator.py:279-285).
  * A_host: n*n host matrix, row-major A[i*n+j]. */

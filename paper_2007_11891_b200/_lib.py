@@ -52,6 +52,7 @@ SIGNATURES = {
     "hdgb_ctx_n_faces": (_I64, [_VP, ctypes.c_int]),
     "hdgb_op_apply": (ctypes.c_int, [_VP, ctypes.c_int, _VP, _VP, _VP]),
     "hdgb_op_apply_host": (ctypes.c_int, [_VP, ctypes.c_int, _VP, _VP, _VP]),
+    "hdgb_op_apply_host_packed": (ctypes.c_int, [_VP, ctypes.c_int, _VP, _VP, _VP]),
     "hdgb_face_transform": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "hdgb_prec_apply": (ctypes.c_int, [_VP, ctypes.c_int, _VP, _VP, _VP]),
     "hdgb_diag_apply": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),

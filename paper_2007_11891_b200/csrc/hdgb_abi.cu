@@ -314,6 +314,23 @@ int hdgb_op_apply_host(hdgb_ctx* c, int variant, const double* u_host, double* r
   return HDGB_OK;
 }
 
+int hdgb_op_apply_host_packed(hdgb_ctx* c, int variant, const double* v_host, double* r_host, void* stream) {
+  if (!c || !v_host || !r_host) return einval("null argument");
+  if (variant != HDGB_PLAIN && variant != HDGB_TRANSFORMED) return einval("unknown operator variant");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!c->d_io) HDGB_CUDA(cudaMalloc(&c->d_io, sizeof(double) * 2 * c->vstride));
+  const size_t bytes = sizeof(double) * c->n_unknown;
+  double* a = c->d_io;                // all-face input, then packed output
+  double* b = c->d_io + c->vstride;   // packed input, then all-face output
+  HDGB_CUDA(cudaMemcpyAsync(b, v_host, bytes, cudaMemcpyHostToDevice, s));
+  HDGB_CUDA(launch_pack(c, 1, b, a, s));  // unpack_unknowns: Dirichlet slots zero
+  HDGB_CUDA(launch_op(c, variant, MODE_APPLY, a, b, s));
+  HDGB_CUDA(launch_pack(c, 0, b, a, s));  // pack_unknowns
+  HDGB_CUDA(cudaMemcpyAsync(r_host, a, bytes, cudaMemcpyDeviceToHost, s));
+  HDGB_CUDA(cudaStreamSynchronize(s));
+  return HDGB_OK;
+}
+
 int hdgb_face_transform(hdgb_ctx* c, const double* A_host, const double* in, double* out, void* stream) {
   if (!c || !A_host || !in || !out) return einval("null argument");
   if (in == out) return einval("input and output must not alias");

@@ -518,18 +518,22 @@ __device__ __forceinline__ int64_t packed_face(const Geo& g, int d, int64_t f) {
 
 template <int MODE>  // 0 pack, 1 unpack, 2 zero dirichlet
 __global__ void pack_kernel(Geo g, int N2, int64_t nfaces, const double* in, double* out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nfaces * N2;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t fid = i / N2;
-    int q = (int)(i - fid * N2);
-    int d = fid >= g.foff[2] ? 2 : (fid >= g.foff[1] ? 1 : 0);
-    int64_t pf = packed_face(g, d, fid - g.foff[d]);
-    if (MODE == 0) {
-      if (pf >= 0) out[pf * N2 + q] = in[i];
-    } else if (MODE == 1) {
-      out[i] = pf >= 0 ? in[pf * N2 + q] : 0.0;
-    } else {
-      if (pf < 0) out[i] = 0.0;
+  // one warp per face: the face -> packed-face map is computed once per face
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t fid = w0; fid < nfaces; fid += nw) {
+    const int d = fid >= g.foff[2] ? 2 : (fid >= g.foff[1] ? 1 : 0);
+    const int64_t pf = packed_face(g, d, fid - g.foff[d]);
+    const int64_t a0 = fid * N2, p0 = pf * N2;
+    for (int q = lane; q < N2; q += 32) {
+      if (MODE == 0) {
+        if (pf >= 0) out[p0 + q] = in[a0 + q];
+      } else if (MODE == 1) {
+        out[a0 + q] = pf >= 0 ? in[p0 + q] : 0.0;
+      } else {
+        if (pf < 0) out[a0 + q] = 0.0;
+      }
     }
   }
 }

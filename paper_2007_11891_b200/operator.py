@@ -225,6 +225,15 @@ class DeviceContext:
         _lib.check(_lib.lib().hdgb_op_apply(self.handle, variant, self.check_vec(u), self.check_vec(r), self.stream()))
         return r
 
+    def apply_host_packed(self, v_host, r_host, variant):
+        """apply_K on packed unknown vectors with host buffers (pinned for full PCIe speed)."""
+        for a in (v_host, r_host):
+            if not (a.dtype == np.float64 and a.flags.c_contiguous and a.size == self.n_unknown):
+                raise ValueError(f"expected contiguous float64 host arrays of length {self.n_unknown}")
+        _lib.check(_lib.lib().hdgb_op_apply_host_packed(self.handle, variant, ctypes.c_void_p(v_host.ctypes.data),
+                                                        ctypes.c_void_p(r_host.ctypes.data), self.stream()))
+        return r_host
+
     def apply_host(self, u_host, r_host, variant):
         """r = K u with host buffers (copies inside; pinned buffers for full PCIe rate)."""
         for a in (u_host, r_host):

@@ -357,3 +357,16 @@ def test_small_and_flat_grids_match_oracle(n_el, p):
                           F, np.zeros_like(F))
     assert conv and abs(it - ito) <= 1, (it, ito)
     assert relerr(x, xo) < 1e-9
+
+
+def test_packed_host_apply_matches_reference_closure():
+    """hdgb_op_apply_host_packed == the reference's apply_K closure on packed vectors."""
+    g = load("cfg1")
+    mesh, ctx = _mesh_ctx(g)
+    dc = hb.device_context(ctx)
+    v = np.ascontiguousarray(g["v"], dtype=np.float64)
+    r = np.empty_like(v)
+    dc.apply_host_packed(v, r, 0)
+    assert relerr(r, g["K_plain_v"]) < TOL
+    dc.apply_host_packed(v, r, 1)
+    assert relerr(r, g["K_trans_v"]) < TOL
