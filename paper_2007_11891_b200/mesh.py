@@ -276,10 +276,6 @@ def scatter_add_batched(blocks, field, include_dirichlet=True):
             field.data[d][hi[kh]] += blk[:, 1][kh]
 
 
-def _is_device(x):
-    return hasattr(x, "is_cuda") or isinstance(x, DeviceFluxField)
-
-
 def pack_unknowns(field):
     """Flatten the unknown face blocks (numpy for host fields, CUDA tensor for device fields)."""
     if isinstance(field, DeviceFluxField):
