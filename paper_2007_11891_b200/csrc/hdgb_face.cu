@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(256) pw_kernel(FaceArgs a, const uint8_t* __re
 //    <p, w> and alpha in CG mode (one fixed-order reduction per kernel).
 enum { FX_TRANSFORM = 0, FX_POST = 1, FX_PREC = 2, FX_INIT = 3, FX_UPDATE = 4 };
 
-template <int N, int FK>
+template <int N, int FK, int CG = 0>
 struct FxCfg {
   static constexpr int N2 = N * N;
   // warps per face group: the smallest of 1, 2, 4 keeping >= 80 % of the lanes on a line,
@@ -168,10 +168,11 @@ struct FxCfg {
   static constexpr int EPT = (FPW * N2 + GT - 1) / GT;  // epilogue values per thread
   // FX_POST stages u next to G with the same bulk copies for N <= 11 (measured: p = 8 plain
   // 446 -> 420 us with 3 CTAs/SM); larger N prefetch u into registers (p = 12/16 faster)
+  // (inside the PCG, CG = 1, the register-prefetch variant measured faster: 941 -> 886 us/iter)
 #ifdef HDGB_FX_POST_TMA
   static constexpr int OPS = (FK == FX_POST && HDGB_FX_POST_TMA) ? 2 : 1;
 #else
-  static constexpr int OPS = (FK == FX_POST && N <= 11) ? 2 : 1;
+  static constexpr int OPS = (FK == FX_POST && !CG && N <= 11) ? 2 : 1;
 #endif
   static constexpr bool BLOCK = FK == FX_PREC || FK == FX_INIT || FK == FX_UPDATE;
   // per-group slice, 128-byte aligned (bulk-copy destinations need 16)
@@ -179,13 +180,14 @@ struct FxCfg {
   static constexpr int YT = BLOCK ? 9 * N2 : 0;      // uniform-grid y^-1 class tables
   static constexpr int smem_doubles() { return NG * per_group() + (YT + 1) / 2 * 2; }
   // register budget (resident CTAs per SM), measured on the config-3 sweep: 3 for the block
-  // preconditioner at N >= 8 (p = 8: 130 -> 116 us) and for the staged plain epilogue; 2 for the
-  // plain pre-transform, where more resident CTAs raised DRAM traffic (L2 thrashing between
-  // the staged reads and the write-back) more than they hid latency.  HDGB_FX_MINB overrides.
+  // preconditioner apply at N >= 8 (p = 8: 130 -> 116 us) and for the staged plain epilogue; 2 for
+  // the plain pre-transform and for the PCG variants (p = 8 block PCG 941 -> 880 us/iter),
+  // where more resident CTAs raised DRAM traffic more than they hid latency.  HDGB_FX_MINB
+  // overrides.
 #ifdef HDGB_FX_MINB
   static constexpr int MINB = HDGB_FX_MINB;
 #else
-  static constexpr int MINB = ((FK == FX_POST && OPS == 2) || (BLOCK && N >= 8)) ? 3 : 2;
+  static constexpr int MINB = ((FK == FX_POST && OPS == 2) || (FK == FX_PREC && N >= 8)) ? 3 : 2;
 #endif
 };
 
@@ -241,10 +243,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 template <int N, int FK, int CG>
-__global__ void __launch_bounds__(FxCfg<N, FK>::NT, (FxCfg<N, FK>::MINB)) fx_kernel(const FaceArgs a, const uint8_t* __restrict__ finfo,
+__global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)) fx_kernel(const FaceArgs a, const uint8_t* __restrict__ finfo,
                                                                      const double* __restrict__ fcoef,
                                                                      const __grid_constant__ FxMats<N> M) {
-  using C = FxCfg<N, FK>;
+  using C = FxCfg<N, FK, CG>;
   constexpr int N2 = C::N2, FPW = C::FPW, NP = C::NP, WP = C::WP, BATW = C::BATW, S = C::S, GT = C::GT;
   constexpr int GW = C::GW, EPT = C::EPT, OPS = C::OPS;
   constexpr bool UTMA = OPS == 2;
@@ -767,7 +769,7 @@ static cudaError_t pw_prec(hdgb_ctx* c, int prec, const FaceArgs& a, cudaStream_
 template <int N, int FK, int CG = 0>
 static cudaError_t fx_launch(hdgb_ctx* c, const FaceArgs& a, const double* Ah, const double* Bh, int nb_b,
                              cudaStream_t s) {
-  using C = FxCfg<N, FK>;
+  using C = FxCfg<N, FK, CG>;
   FxMats<N> M;
   for (int q = 0; q < N * N; ++q) {
     M.A[q] = Ah[q];
