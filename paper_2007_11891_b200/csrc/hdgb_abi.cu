@@ -62,6 +62,9 @@ static void free_ctx(hdgb_ctx* c) {
   for (auto& row : c->graph)
     for (auto& gx : row)
       if (gx) cudaGraphExecDestroy(gx);
+  for (auto& row : c->io_graph)
+    for (auto& ig : row)
+      if (ig.exec) cudaGraphExecDestroy(ig.exec);
   double* bufs[] = {c->d_tab, c->d_dz, c->d_widths, c->d_yinv_cls, c->d_y_cls, c->d_dn_cls, c->d_yinv_full,
                     c->d_y_full, c->d_dn_full, c->d_hat, c->d_part, c->d_fcoef, c->d_vec, c->d_io};
   for (double* b : bufs)
@@ -301,34 +304,85 @@ int hdgb_op_apply(hdgb_ctx* c, int variant, const double* u, double* r, void* st
   return HDGB_OK;
 }
 
+// H2D, (unpack,) apply, (pack,) D2H on stream s
+static cudaError_t enqueue_host_apply(hdgb_ctx* c, int variant, int packed, const double* v_host, double* r_host,
+                                      cudaStream_t s) {
+  const size_t bytes = sizeof(double) * (packed ? c->n_unknown : c->n_all);
+  double* a = c->d_io;               // input (packed: all-face input, then packed output)
+  double* b = c->d_io + c->vstride;  // output (packed: packed input, then all-face output)
+  cudaError_t e;
+  if (packed) {
+    if ((e = cudaMemcpyAsync(b, v_host, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
+    if ((e = launch_pack(c, 1, b, a, s)) != cudaSuccess) return e;  // unpack_unknowns: Dirichlet slots zero
+    if ((e = launch_op(c, variant, MODE_APPLY, a, b, s)) != cudaSuccess) return e;
+    if ((e = launch_pack(c, 0, b, a, s)) != cudaSuccess) return e;  // pack_unknowns
+    return cudaMemcpyAsync(r_host, a, bytes, cudaMemcpyDeviceToHost, s);
+  }
+  if ((e = cudaMemcpyAsync(a, v_host, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
+  if ((e = launch_op(c, variant, MODE_APPLY, a, b, s)) != cudaSuccess) return e;
+  return cudaMemcpyAsync(r_host, b, bytes, cudaMemcpyDeviceToHost, s);
+}
+
+static bool pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// Pinned host buffers: the whole sequence replays as one CUDA graph (one host call instead of
+// one per copy and kernel; the captured launches keep their programmatic-dependency edges).
+// Pageable buffers take the stream path (staged copies cannot be captured).
+static int host_apply(hdgb_ctx* c, int variant, int packed, const double* v_host, double* r_host, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!c->d_io) HDGB_CUDA(cudaMalloc(&c->d_io, sizeof(double) * 2 * c->vstride));
+  if (!(pinned(v_host) && pinned(r_host))) {
+    HDGB_CUDA(enqueue_host_apply(c, variant, packed, v_host, r_host, s));
+    HDGB_CUDA(cudaStreamSynchronize(s));
+    return HDGB_OK;
+  }
+  hdgb_ctx::IoGraph& ig = c->io_graph[variant][packed];
+  if (!ig.exec || ig.v != v_host || ig.r != r_host) {
+    if (ig.exec) cudaGraphExecDestroy(ig.exec);
+    ig.exec = nullptr;
+    const int64_t l0 = c->launches;
+    HDGB_CUDA(cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
+    cudaError_t ke = enqueue_host_apply(c, variant, packed, v_host, r_host, c->s);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(c->s, &graph);
+    if (ke != cudaSuccess || e != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      return cuda_fail(ke != cudaSuccess ? ke : e, "host apply capture");
+    }
+    e = cudaGraphInstantiate(&ig.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+      ig.exec = nullptr;
+      return cuda_fail(e, "cudaGraphInstantiate(host apply)");
+    }
+    ig.launches = c->launches - l0;
+    c->launches = l0;
+    ig.v = v_host;
+    ig.r = r_host;
+  }
+  HDGB_CUDA(cudaGraphLaunch(ig.exec, s));
+  c->launches += ig.launches;
+  HDGB_CUDA(cudaStreamSynchronize(s));
+  return HDGB_OK;
+}
+
 int hdgb_op_apply_host(hdgb_ctx* c, int variant, const double* u_host, double* r_host, void* stream) {
   if (!c || !u_host || !r_host) return einval("null argument");
   if (variant != HDGB_PLAIN && variant != HDGB_TRANSFORMED) return einval("unknown operator variant");
-  cudaStream_t s = (cudaStream_t)stream;
-  if (!c->d_io) HDGB_CUDA(cudaMalloc(&c->d_io, sizeof(double) * 2 * c->vstride));
-  const size_t bytes = sizeof(double) * c->n_all;
-  HDGB_CUDA(cudaMemcpyAsync(c->d_io, u_host, bytes, cudaMemcpyHostToDevice, s));
-  HDGB_CUDA(launch_op(c, variant, MODE_APPLY, c->d_io, c->d_io + c->vstride, s));
-  HDGB_CUDA(cudaMemcpyAsync(r_host, c->d_io + c->vstride, bytes, cudaMemcpyDeviceToHost, s));
-  HDGB_CUDA(cudaStreamSynchronize(s));
-  return HDGB_OK;
+  return host_apply(c, variant, 0, u_host, r_host, stream);
 }
 
 int hdgb_op_apply_host_packed(hdgb_ctx* c, int variant, const double* v_host, double* r_host, void* stream) {
   if (!c || !v_host || !r_host) return einval("null argument");
   if (variant != HDGB_PLAIN && variant != HDGB_TRANSFORMED) return einval("unknown operator variant");
-  cudaStream_t s = (cudaStream_t)stream;
-  if (!c->d_io) HDGB_CUDA(cudaMalloc(&c->d_io, sizeof(double) * 2 * c->vstride));
-  const size_t bytes = sizeof(double) * c->n_unknown;
-  double* a = c->d_io;                // all-face input, then packed output
-  double* b = c->d_io + c->vstride;   // packed input, then all-face output
-  HDGB_CUDA(cudaMemcpyAsync(b, v_host, bytes, cudaMemcpyHostToDevice, s));
-  HDGB_CUDA(launch_pack(c, 1, b, a, s));  // unpack_unknowns: Dirichlet slots zero
-  HDGB_CUDA(launch_op(c, variant, MODE_APPLY, a, b, s));
-  HDGB_CUDA(launch_pack(c, 0, b, a, s));  // pack_unknowns
-  HDGB_CUDA(cudaMemcpyAsync(r_host, a, bytes, cudaMemcpyDeviceToHost, s));
-  HDGB_CUDA(cudaStreamSynchronize(s));
-  return HDGB_OK;
+  return host_apply(c, variant, 1, v_host, r_host, stream);
 }
 
 int hdgb_face_transform(hdgb_ctx* c, const double* A_host, const double* in, double* out, void* stream) {

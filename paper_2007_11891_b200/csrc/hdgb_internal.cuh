@@ -280,6 +280,14 @@ struct hdgb_ctx {
   cudaStream_t s = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaGraphExec_t graph[2][4] = {{nullptr}};
+  // host-buffer applies on pinned memory: one captured graph per (variant, packed), keyed by
+  // the host pointers it was captured with
+  struct IoGraph {
+    cudaGraphExec_t exec = nullptr;
+    const void* v = nullptr;
+    void* r = nullptr;
+    int64_t launches = 0;
+  } io_graph[2][2];
   int64_t launches = 0;
   // L2 working-set target of one z-slab of the colour passes; 0 = one slab.  Slabbing cuts
   // HBM traffic (pass-0 partials stay in L2) but multiplies launches; while the element

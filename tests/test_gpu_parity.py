@@ -370,3 +370,29 @@ def test_packed_host_apply_matches_reference_closure():
     assert relerr(r, g["K_plain_v"]) < TOL
     dc.apply_host_packed(v, r, 1)
     assert relerr(r, g["K_trans_v"]) < TOL
+
+
+def test_pinned_host_apply_graph_replay():
+    """Pinned host buffers take the captured-graph path: bitwise equal to the pageable stream path,
+    fresh data on replay, re-capture when the buffers change."""
+    import torch
+
+    g = load("cfg1")
+    mesh, ctx = _mesh_ctx(g)
+    dc = hb.device_context(ctx)
+    rng = np.random.default_rng(7)
+    pin = [torch.empty(dc.n_unknown, dtype=torch.float64).pin_memory().numpy() for _ in range(4)]
+    for variant in (0, 1):
+        for step in range(3):
+            v = rng.uniform(-1, 1, dc.n_unknown)
+            want = dc.apply_host_packed(v, np.empty_like(v), variant)  # pageable: stream path
+            vi, ri = (pin[0], pin[1]) if step < 2 else (pin[2], pin[3])
+            vi[:] = v
+            dc.apply_host_packed(vi, ri, variant)
+            assert np.array_equal(ri, want), (variant, step)
+        hall = [torch.empty(dc.n_all, dtype=torch.float64).pin_memory().numpy() for _ in range(2)]
+        u = dc.unpack(torch.from_numpy(rng.uniform(-1, 1, dc.n_unknown)).cuda()).cpu().numpy()
+        want = dc.apply_host(u, np.empty_like(u), variant)
+        hall[0][:] = u
+        dc.apply_host(hall[0], hall[1], variant)
+        assert np.array_equal(hall[1], want)
