@@ -201,12 +201,13 @@ def _timed_apply(dc, u, r, variant, steps, warmup, flush, stream):
     return ms, dc.launches() - l0
 
 
-def _large_point(hb, p, m, lam, flush, stream, hbm, fp64_peak, reps=10):
-    """Apply timings (plain, transformed, block and eigen-diagonal preconditioners) on an m^3 grid."""
+def _large_point(hb, p, m, lam, flush, stream, hbm, fp64_peak, reps=10, mesh=None, cfg=None):
+    """Apply timings (plain, transformed, block and eigen-diagonal preconditioners) on an m^3 grid
+    (or on `mesh` with `cfg`)."""
     import torch
 
-    mesh = hb.Mesh((m, m, m))
-    ctx = hb.make_context(mesh, p, hb.SolverConfig(lam=lam))
+    mesh = mesh or hb.Mesh((m, m, m))
+    ctx = hb.make_context(mesh, p, cfg or hb.SolverConfig(lam=lam))
     dc = hb.device_context(ctx)
     n = p + 1
     N, N_all = mesh.n_trace_unknowns(p), mesh.n_all(p)
@@ -260,6 +261,53 @@ def _large_point(hb, p, m, lam, flush, stream, hbm, fp64_peak, reps=10):
         out[name] = {"us_per_iter": t_it * 1e6, "ps_per_unknown_per_iter": t_it / N * 1e12,
                      "hbm_frac_of_96B_per_unknown": 96 * N_all / t_it / 1e9 / hbm, "iterations": it}
     del dc, ctx, u, r
+    torch.cuda.empty_cache()
+    return out
+
+
+def _config4(hb, flush, stream, hbm, fp64_peak):
+    """non-uniform 64x32x32 grid on [0,2]x[0,1]^2, p = 7, lambda = 100, per-axis
+    widths uniform[0.5, 2] x mean from rng(7) (x, y, z order) rescaled to the box, tau_hat = 0.390625
+    ("reference" convention); apply / PCG-iteration timings plus a full solve() of
+    u = cos(pi x) sin(2 pi y) sin(pi z) (f = (100 + 6 pi^2) u, inhomogeneous Dirichlet data on x = 0, 2)."""
+    import torch
+
+    n, L, p = (64, 32, 32), (2.0, 1.0, 1.0), 7
+    rng = np.random.default_rng(7)
+    widths = []
+    for d in range(3):
+        w = rng.uniform(0.5, 2.0, n[d]) * (L[d] / n[d])
+        widths.append(w * (L[d] / w.sum()))
+    mesh = hb.Mesh(n, (0.0, 0.0, 0.0), L, "dirichlet", widths=widths)
+    cfg = hb.SolverConfig(lam=100.0, tau=0.390625, tau_convention="reference")
+    out = _large_point(hb, p, None, None, flush, stream, hbm, fp64_peak, mesh=mesh, cfg=cfg)
+    ctx = hb.make_context(mesh, p, cfg)
+    pi = math.pi
+
+    def exact(x1, x2, x3):
+        return np.cos(pi * x1) * np.sin(2 * pi * x2) * np.sin(pi * x3)
+
+    X = mesh.element_node_grids(ctx.basis.nodes)
+    shape = (mesh.n_elements,) + (p + 1,) * 3
+    u_ex = np.broadcast_to(exact(*X), shape)
+    f = np.ascontiguousarray((100.0 + 6 * pi * pi) * u_ex)
+    g_D = hb.FluxField(mesh, p)
+    for d in range(3):
+        m = mesh.face_kind[d] == hb.DIRICHLET
+        if np.any(m):
+            g_D.data[d][m] = np.broadcast_to(exact(*mesh.face_node_grids(d, ctx.basis.nodes)), g_D.data[d].shape)[m]
+    u0 = np.zeros(shape)
+    hb.solve(u0, f, g_D, None, cfg, ctx)  # warm-up (graph capture)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    u, _, rep = hb.solve(u0, f, g_D, None, cfg, ctx)
+    wall = time.perf_counter() - t0
+    out["solve"] = {"iterations": rep.iterations, "converged": rep.converged, "relres": rep.relative_residual,
+                    "pcg_ms": rep.wall_time * 1e3, "wall_ms": wall * 1e3,
+                    "us_per_unknown_per_iter": rep.wall_time / max(rep.iterations, 1) / out["trace_unknowns"] * 1e6,
+                    "err_max": float(np.max(np.abs(u - u_ex)))}
+    out["mesh"] = "64x32x32 non-uniform on [0,2]x[0,1]^2, p=7, lambda=100, tau_hat=0.390625"
+    del ctx
     torch.cuda.empty_cache()
     return out
 
@@ -538,6 +586,8 @@ def run_ours(args):
         ps = [2, 3, 4, 6, 8, 12, 16] if args.sweep else [8]
         for p3 in ps:
             large[f"config3_p{p3}"] = _large_point(hb, p3, sizes[p3], 0.0, flush, stream, hbm, fp64_peak.value)
+        if args.sweep or args.config4:
+            large["config4_64x32x32_p7_nonuniform"] = _config4(hb, flush, stream, hbm, fp64_peak.value)
         if args.config5:
             large["config5_128^3_p8"] = _large_point(hb, 8, 128, 1.0, flush, stream, hbm, fp64_peak.value, reps=5)
 
@@ -597,6 +647,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-large", action="store_true", help="skip the config-3 (p=8, 44^3) measurement")
     ap.add_argument("--sweep", action="store_true", help="full config-3 degree sweep p=2..16")
+    ap.add_argument("--config4", action="store_true", help="also time config 4 (64x32x32 non-uniform, p=7)")
     ap.add_argument("--config5", action="store_true", help="also time config 5 (128^3, p=8, 4 GB vectors)")
     args = ap.parse_args()
     if args.impl == "reference":
