@@ -517,6 +517,15 @@ static cudaError_t enqueue_iteration(hdgb_ctx* c, int variant, int prec, cudaGra
   double* v = c->d_vec;
   const int64_t n = c->n_all;
   cudaError_t e;
+  if (variant == HDGB_PLAIN) {
+    // p = z + beta p fused into the operator's pre-transform (beta = 0 before the first
+    // iteration); w = K p with <p, w> and alpha from the epilogue; the x, r update ends the loop
+    c->pupd_z = v + V_Z * c->vstride;
+    e = launch_op(c, variant, MODE_CG, v + V_P * c->vstride, v + V_W * c->vstride, c->s);
+    c->pupd_z = nullptr;
+    if (e != cudaSuccess) return e;
+    return launch_cg_update(c, prec, c->s, h, has_loop);  // x,r update; z = P r; ||r||, <r,z>
+  }
   // w = K p with <p, w> and alpha finished by the operator's last kernel
   if ((e = launch_op(c, variant, MODE_CG, v + V_P * c->vstride, v + V_W * c->vstride, c->s)) != cudaSuccess) return e;
   if ((e = launch_cg_update(c, prec, c->s)) != cudaSuccess) return e;  // x,r update; z = P r; ||r||, <r,z>
@@ -551,7 +560,10 @@ static int build_graph(hdgb_ctx* c, int variant, int prec) {
     cudaGraphDestroy(graph);
     return cuda_fail(e, "cudaStreamBeginCaptureToGraph");
   }
+  const int64_t l0 = c->launches;
   cudaError_t ke = enqueue_iteration(c, variant, prec, h, 1);
+  c->graph_launches[variant][prec] = c->launches - l0;  // kernels per iteration
+  c->launches = l0;
   cudaGraph_t captured;
   e = cudaStreamEndCapture(c->s, &captured);
   if (ke != cudaSuccess || e != cudaSuccess) {
@@ -604,7 +616,6 @@ int hdgb_pcg(hdgb_ctx* c, int variant, int prec, const double* F, double* x, dou
         if (rc != HDGB_OK) return rc;
       }
       HDGB_CUDA(cudaGraphLaunch(c->graph[variant][prec], c->s));
-      c->launches += 4;  // per iteration (counted again below)
     } else {
       // host-driven loop (debug): one iteration per round trip
       for (int it = 0; it < max_iters; ++it) {
@@ -620,7 +631,7 @@ int hdgb_pcg(hdgb_ctx* c, int variant, int prec, const double* F, double* x, dou
     }
     HDGB_CUDA(cudaMemcpyAsync(h, c->d_st, sizeof(CGState), cudaMemcpyDeviceToHost, c->s));
     HDGB_CUDA(cudaStreamSynchronize(c->s));
-    if (use_graph) c->launches += 4LL * (h->it > 0 ? h->it - 1 : 0);
+    if (use_graph) c->launches += c->graph_launches[variant][prec] * (int64_t)(h->it > 0 ? h->it : 1);
   }
   HDGB_CUDA(cudaMemcpyAsync(x, v + V_X * c->vstride, bytes, cudaMemcpyDeviceToDevice, c->s));
   HDGB_CUDA(cudaEventRecord(c->ev_out, c->s));

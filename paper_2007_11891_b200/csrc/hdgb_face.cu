@@ -38,7 +38,10 @@ __global__ void __launch_bounds__(256) pw_kernel(FaceArgs a, const uint8_t* __re
   constexpr unsigned N2 = N * N;
   pdl_trigger();
   pdl_wait();
-  if (FK != PW_PREC && a.st->done) return;
+  if (FK != PW_PREC && a.st->done) {
+    if (FK == PW_UPDATE && a.loop_on && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(a.loop, 0u);
+    return;
+  }
   const double alpha = FK == PW_UPDATE ? a.st->alpha : 0.0;
   double rr = 0.0, rz = 0.0;
   const unsigned stride = gridDim.x * 256u * PW_U;
@@ -109,6 +112,7 @@ __global__ void __launch_bounds__(256) pw_kernel(FaceArgs a, const uint8_t* __re
         CGState* st = a.st;
         if (FK == PW_INIT) cg_init_r(st, trr);
         else cg_update_r(st, trr);
+        if (FK == PW_UPDATE && a.loop_on && st->done) cudaGraphSetConditional(a.loop, 0u);
         if (WITHZ && !st->done) {
           if (FK == PW_INIT) cg_init_z(st, trz);
           else cg_update_z(st, trz);
@@ -170,9 +174,9 @@ struct FxCfg {
   // 446 -> 420 us with 3 CTAs/SM); larger N prefetch u into registers (p = 12/16 faster)
   // (inside the PCG, CG = 1, the register-prefetch variant measured faster: 941 -> 886 us/iter)
 #ifdef HDGB_FX_POST_TMA
-  static constexpr int OPS = (FK == FX_POST && HDGB_FX_POST_TMA) ? 2 : 1;
+  static constexpr int OPS = ((FK == FX_POST && HDGB_FX_POST_TMA) || (FK == FX_TRANSFORM && CG)) ? 2 : 1;
 #else
-  static constexpr int OPS = (FK == FX_POST && !CG && N <= 11) ? 2 : 1;
+  static constexpr int OPS = ((FK == FX_POST && !CG && N <= 11) || (FK == FX_TRANSFORM && CG)) ? 2 : 1;
 #endif
   static constexpr bool BLOCK = FK == FX_PREC || FK == FX_INIT || FK == FX_UPDATE;
   // per-group slice, 128-byte aligned (bulk-copy destinations need 16)
@@ -187,7 +191,14 @@ struct FxCfg {
 #ifdef HDGB_FX_MINB
   static constexpr int MINB = HDGB_FX_MINB;
 #else
-  static constexpr int MINB = ((FK == FX_POST && OPS == 2) || (FK == FX_PREC && N >= 8)) ? 3 : 2;
+#ifndef HDGB_FXU_MINB
+#define HDGB_FXU_MINB 2
+#endif
+#ifndef HDGB_FXT_MINB
+#define HDGB_FXT_MINB 2
+#endif
+  static constexpr int MINB = ((FK == FX_POST && OPS == 2) || (FK == FX_PREC && N >= 8)) ? 3
+                              : (FK == FX_UPDATE ? HDGB_FXU_MINB : (FK == FX_TRANSFORM && CG ? HDGB_FXT_MINB : 2));
 #endif
 };
 
@@ -253,12 +264,17 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
   constexpr bool BLOCK = C::BLOCK;
   constexpr bool RED = FK == FX_INIT || FK == FX_UPDATE;
   constexpr bool POST = FK == FX_POST;
+  // plain PCG: the direction update p = z + beta p (solver.py:320) fused into the
+  // pre-transform of the next operator apply: stages z and p, writes p and (T (x) T) p
+  constexpr bool PUPD = FK == FX_TRANSFORM && CG;
   constexpr bool ODD = N & 1;  // row-wise stores N doubles apart are bank-conflict-free
+  constexpr bool EARLY = RED || (POST && CG) || PUPD;  // reads the PCG state first
   pdl_trigger();
-  if (RED || (POST && CG)) {
+  if (EARLY) {
     pdl_wait();
     if (a.st->done) return;
   }
+  const double beta = PUPD ? a.st->beta : 0.0;
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t sBar[C::NG][S];
   __shared__ double sWq[N];  // FX_POST: quadrature weights (dynamic index: keep out of the constant bank)
@@ -277,7 +293,7 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();  // the only CTA-wide barrier: tables and barrier init
-  if (!(RED || (POST && CG))) pdl_wait();  // inputs come from earlier kernels
+  if (!EARLY) pdl_wait();  // inputs come from earlier kernels
   auto gsync = [&]() {
     if (GW == 1) {
       __syncwarp();
@@ -287,6 +303,7 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
   };
   // FX_POST overwrites G (a.out) in place with r; each batch is staged before it is written
   const double* src = POST ? a.out : a.in;
+  const double* src2 = POST ? a.in : a.p;  // second staged operand (UTMA): u, or p
   const int64_t nbat = (a.nfaces + FPW - 1) / FPW;
   const int64_t gg = (int64_t)blockIdx.x * C::NG + grp, ngg = (int64_t)gridDim.x * C::NG;
   const int64_t nmine = gg < nbat ? (nbat - 1 - gg) / ngg + 1 : 0;
@@ -301,11 +318,11 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
     uint64_t* bar = &sBar[grp][k % S];
     if (bulk != total) {
       dst[bulk] = src[lo + bulk];
-      if (UTMA) dst[BATW + bulk] = a.in[lo + bulk];
+      if (UTMA) dst[BATW + bulk] = src2[lo + bulk];
     }
     mbar_expect_tx(bar, bulk * 8u * OPS);
     bulk_g2s(dst, src + lo, bulk * 8u, bar);
-    if (UTMA) bulk_g2s(dst + BATW, a.in + lo, bulk * 8u, bar);
+    if (UTMA) bulk_g2s(dst + BATW, src2 + lo, bulk * 8u, bar);
   };
   if (gl == 0)
     for (int64_t k = 0; k < S - 1 && k < nmine; ++k) issue(k);
@@ -333,8 +350,17 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
     double x[N], y[N], z[N];
     if (on) {  // pass 1 along the first index: column l
       const double* xs = sX + f * N2 + l;
+      if (PUPD) {  // p = z + beta p on column l, kept in the p stage for the epilogue store
+        double* ps = sX + BATW + f * N2 + l;
 #pragma unroll
-      for (int i = 0; i < N; ++i) x[i] = xs[i * N];
+        for (int i = 0; i < N; ++i) {
+          x[i] = fma(beta, ps[i * N], xs[i * N]);
+          ps[i * N] = x[i];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) x[i] = xs[i * N];
+      }
       line_mv<N>(M.A, x, y);
       double* ws = sW + f * WP + l;
 #pragma unroll
@@ -417,6 +443,7 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
       }
       a.out[gi] = v;
       if (FK == FX_INIT) a.p[gi] = v;
+      if (PUPD) a.p[gi] = sX[BATW + it];
     }
     gsync();  // the stage and the tile are reused
   }
@@ -863,6 +890,25 @@ static cudaError_t face_any(hdgb_ctx* c, int op, int prec, const FaceArgs& a, cu
   return cudaErrorInvalidValue;
 }
 
+// plain PCG: p = z + beta p and out = (A (x) A) p in one pass over the faces
+cudaError_t launch_face_transform_pupd(hdgb_ctx* c, const double* A_host, const double* z, double* p, double* out,
+                                       cudaStream_t s) {
+  FaceArgs a = base_args(c, HDGB_PREC_NONE);
+  a.in = z;
+  a.p = p;
+  a.out = out;
+  switch (c->N) {
+#define HDGB_CASE(n) \
+  case n:            \
+    return fx_launch<n, FX_TRANSFORM, 1>(c, a, A_host, nullptr, 0, s);
+    HDGB_CASE(2) HDGB_CASE(3) HDGB_CASE(4) HDGB_CASE(5) HDGB_CASE(6) HDGB_CASE(7) HDGB_CASE(8) HDGB_CASE(9)
+    HDGB_CASE(10) HDGB_CASE(11) HDGB_CASE(12) HDGB_CASE(13) HDGB_CASE(14) HDGB_CASE(15) HDGB_CASE(16)
+    HDGB_CASE(17)
+#undef HDGB_CASE
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_face_transform(hdgb_ctx* c, const double* A_host, const double* in, double* out, cudaStream_t s) {
   FaceArgs a = base_args(c, HDGB_PREC_NONE);
   a.A = A_host;
@@ -910,8 +956,10 @@ cudaError_t launch_cg_init(hdgb_ctx* c, int kind, cudaStream_t s) {
   return face_any(c, OP_CG_INIT, kind, a, s);
 }
 
-cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s) {
+cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s, cudaGraphConditionalHandle loop, int loop_on) {
   FaceArgs a = base_args(c, kind);
+  a.loop = loop;
+  a.loop_on = loop_on;
   double* v = c->d_vec;
   const int64_t n = c->n_all;
   a.x = v + V_X * c->vstride;

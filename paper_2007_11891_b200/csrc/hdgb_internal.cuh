@@ -144,6 +144,8 @@ struct FaceArgs {
   double* z;
   double* part;          // per-CTA partials [gridDim][2]
   CGState* st;
+  cudaGraphConditionalHandle loop;  // PCG graph: the x, r update ends the loop once done
+  int loop_on;
 };
 
 // ---------------------------------------------------------------- deterministic reductions
@@ -219,7 +221,12 @@ __device__ __forceinline__ void cg_init_r(CGState* st, double rr) {  // r0 = F -
     st->relres = 1.0;
   }
 }
-__device__ __forceinline__ void cg_init_z(CGState* st, double rz) { st->rho = rz; st->rz = rz; }
+// beta = 0 before the first iteration: the fused direction update (plain PCG) then gives p = z
+__device__ __forceinline__ void cg_init_z(CGState* st, double rz) {
+  st->rho = rz;
+  st->rz = rz;
+  st->beta = 0.0;
+}
 __device__ __forceinline__ void cg_update_r(CGState* st, double rr) {  // after x += a p, r -= a w
   const double rn = sqrt(rr);
   st->rr = rr;
@@ -276,10 +283,14 @@ struct hdgb_ctx {
   hdgb::CGState* d_st = nullptr;
   hdgb::CGState* h_st = nullptr;  // pinned mirror
   double* d_vec = nullptr;        // CG vectors x r z p w F (6 * n_all)
+  // plain PCG: z slot of the direction update fused into the pre-transform (set around
+  // the operator launch of an iteration; null otherwise)
+  const double* pupd_z = nullptr;
   double* d_io = nullptr;         // host-path staging (2 * n_all)
   cudaStream_t s = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaGraphExec_t graph[2][4] = {{nullptr}};
+  int64_t graph_launches[2][4] = {{0}};  // kernels per PCG iteration of each graph
   // host-buffer applies on pinned memory: one captured graph per (variant, packed), keyed by
   // the host pointers it was captured with
   struct IoGraph {
@@ -303,11 +314,14 @@ int cuda_fail(cudaError_t e, const char* what);
 cudaError_t launch_op(hdgb_ctx* c, int variant, int mode, const double* u, double* r, cudaStream_t s);
 cudaError_t launch_face_transform(hdgb_ctx* c, const double* A_host, const double* in, double* out, cudaStream_t s);
 cudaError_t launch_plain_post(hdgb_ctx* c, int cg, const double* u, double* r, cudaStream_t s);
+cudaError_t launch_face_transform_pupd(hdgb_ctx* c, const double* A_host, const double* z, double* p, double* out,
+                                       cudaStream_t s);
 cudaError_t launch_build_rhs(hdgb_ctx* c, const double* f, double* F, cudaStream_t s);
 cudaError_t launch_hybridize(hdgb_ctx* c, const double* u0, const double* gN, double* x, cudaStream_t s);
 cudaError_t launch_recover(hdgb_ctx* c, const double* f, const double* tr, double* u, double* q, cudaStream_t s);
 cudaError_t launch_prec(hdgb_ctx* c, int kind, const double* in, double* out, cudaStream_t s);
-cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s);
+cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s, cudaGraphConditionalHandle loop = 0,
+                             int loop_on = 0);
 cudaError_t launch_cg_init(hdgb_ctx* c, int kind, cudaStream_t s);
 cudaError_t launch_diag_user(hdgb_ctx* c, const double* diag, const double* in, double* out, cudaStream_t s);
 int grid_for(int64_t work, int per);

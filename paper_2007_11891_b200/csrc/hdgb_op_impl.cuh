@@ -359,7 +359,10 @@ static cudaError_t launch_t(hdgb_ctx* c, const double* u, double* r, cudaStream_
   if (PLAIN) {
     TabOff to;
     to.set(N);
-    cudaError_t e = launch_face_transform(c, c->h_tab.data() + to.T, u, c->d_hat, s);
+    cudaError_t e = (MODE & 1) && c->pupd_z
+                        ? launch_face_transform_pupd(c, c->h_tab.data() + to.T, c->pupd_z, const_cast<double*>(u),
+                                                     c->d_hat, s)
+                        : launch_face_transform(c, c->h_tab.data() + to.T, u, c->d_hat, s);
     if (e != cudaSuccess) return e;
     a.u = c->d_hat;
   }
