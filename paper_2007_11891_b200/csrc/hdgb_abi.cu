@@ -517,19 +517,14 @@ static cudaError_t enqueue_iteration(hdgb_ctx* c, int variant, int prec, cudaGra
   double* v = c->d_vec;
   const int64_t n = c->n_all;
   cudaError_t e;
-  if (variant == HDGB_PLAIN) {
-    // p = z + beta p fused into the operator's pre-transform (beta = 0 before the first
-    // iteration); w = K p with <p, w> and alpha from the epilogue; the x, r update ends the loop
-    c->pupd_z = v + V_Z * c->vstride;
-    e = launch_op(c, variant, MODE_CG, v + V_P * c->vstride, v + V_W * c->vstride, c->s);
-    c->pupd_z = nullptr;
-    if (e != cudaSuccess) return e;
-    return launch_cg_update(c, prec, c->s, h, has_loop);  // x,r update; z = P r; ||r||, <r,z>
-  }
-  // w = K p with <p, w> and alpha finished by the operator's last kernel
-  if ((e = launch_op(c, variant, MODE_CG, v + V_P * c->vstride, v + V_W * c->vstride, c->s)) != cudaSuccess) return e;
-  if ((e = launch_cg_update(c, prec, c->s)) != cudaSuccess) return e;  // x,r update; z = P r; ||r||, <r,z>
-  return launch_p_update(c, c->s, h, has_loop);                        // p = z + beta p; loop control
+  // p = z + beta p fused into the operator (beta = 0 before the first iteration, when p = z
+  // already): the plain pre-transform, or the transformed colour passes; w = K p with <p, w>
+  // and alpha from the operator's last kernel; the x, r update ends the loop once done
+  c->pupd_z = v + V_Z * c->vstride;
+  e = launch_op(c, variant, MODE_CG, v + V_P * c->vstride, v + V_W * c->vstride, c->s);
+  c->pupd_z = nullptr;
+  if (e != cudaSuccess) return e;
+  return launch_cg_update(c, prec, c->s, h, has_loop);  // x,r update; z = P r; ||r||, <r,z>
 }
 
 // Build (once per variant/prec) a graph whose conditional WHILE node runs PCG iterations

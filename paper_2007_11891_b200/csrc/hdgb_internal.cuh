@@ -122,6 +122,8 @@ struct OpArgs {
   int uniform;
   CGState* st;           // CG mode: early-exit flag, <p, w>
   double* part;          // CG mode: per-CTA partials of <p, w>
+  const double* z;       // CG mode, fused direction update: z (u = p is updated in place via pout)
+  double* pout;
 };
 
 struct FaceArgs {

@@ -116,7 +116,10 @@ struct OpVCfg {
 #else
   static constexpr bool DZS = N >= 12;
 #endif
-  __host__ __device__ static constexpr int smem_doubles() { return G * (2 * FS + VS) + (DZS ? N * NQ : 0); }
+  // PUPD (transformed PCG, direction update fused into colour pass 0): z staged next to p
+  __host__ __device__ static constexpr int smem_doubles(bool pupd = false) {
+    return G * (2 * FS + VS) + (DZS ? N * NQ : 0) + (pupd ? 2 * G * FS : 0);
+  }
 };
 
 // 1D reference-element tables as kernel parameters (constant bank): every compile-time
@@ -144,10 +147,16 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
   using C = OpVCfg<N>;
   constexpr int NQ = C::NQ, G = C::G, FS = C::FS, VS = C::VS;
   constexpr bool UNI = !(MODE & 2), CG = MODE & 1, GONLY = MODE & 4;
+  // bit 3 (CG only): p = z + beta p (solver.py:320) fused into the staging of this pass: colour 0
+  // updates every face of its elements, colour 1 the faces it alone touches (the rest already
+  // hold the new p); the new p is written back for the x update
+  constexpr bool PUPD = CG && (MODE & 8);
   pdl_trigger();
+  double beta = 0.0;
   if (CG) {
     pdl_wait();
     if (a.st->done) return;
+    if (PUPD) beta = a.st->beta;
   }
   extern __shared__ __align__(16) double smem[];
   double* sF0 = smem;              // 2 x G x [6][NQ] staged faces
@@ -197,11 +206,18 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
       }
     }
   };
-  auto stage = [&](const ElemInfo* inf, double* buf) {
+  double* sZ0 = smem + G * (2 * FS + VS) + (C::DZS ? N * NQ : 0);  // PUPD: 2 x G x [6][NQ] staged z
+  auto stage = [&](const ElemInfo* inf, double* buf, int bi) {
     if (act && inf[e].valid) {
       double* dst = buf + e * FS + q;
 #pragma unroll
       for (int s = 0; s < 6; ++s) cp_async8(dst + s * NQ, a.u + (inf[e].off[s] + (unsigned)q));
+      if (PUPD) {
+        double* dz = sZ0 + bi * G * FS + e * FS + q;
+#pragma unroll
+        for (int s = 0; s < 6; ++s)
+          if (COLOR == 0 || !(inf[e].shared >> s & 1u)) cp_async8(dz + s * NQ, a.z + (inf[e].off[s] + (unsigned)q));
+      }
     }
   };
 
@@ -210,17 +226,16 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
   if (gi < ngroups) info(gi, sInfo[0]);
   __syncthreads();
   if (!CG) pdl_wait();  // u and r come from earlier kernels
-  if (gi < ngroups) stage(sInfo[0], sF0);
+  if (gi < ngroups) stage(sInfo[0], sF0, 0);
   cp_async_commit();
   for (int buf = 0; gi < ngroups; gi += gridDim.x, buf ^= 1) {
     const int64_t gn = gi + gridDim.x;
     if (gn < ngroups) info(gn, sInfo[buf ^ 1]);
     __syncthreads();
-    if (gn < ngroups) stage(sInfo[buf ^ 1], sF0 + (buf ^ 1) * G * FS);
+    if (gn < ngroups) stage(sInfo[buf ^ 1], sF0 + (buf ^ 1) * G * FS, buf ^ 1);
     cp_async_commit();
     asm volatile("cp.async.wait_group 1;\n" ::);
-    __syncthreads();
-    // element geometry into registers once
+    // element geometry into registers once (sInfo[buf] was published a barrier ago)
     const ElemInfo& I = sInfo[buf][act ? e : 0];
     const bool on = act && I.valid;
     unsigned off[6];
@@ -232,8 +247,21 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
     }
     const unsigned shared = I.shared;
     const double al0 = I.al[0], al1 = I.al[1], al2 = I.al[2], al3 = I.al[3];
-    const double* sF = sF0 + buf * G * FS + (act ? e : 0) * FS;
+    double* sFw = sF0 + buf * G * FS + (act ? e : 0) * FS;
+    const double* sF = sFw;
     double* vU = sU + (act ? e : 0) * VS;
+    if (PUPD && on) {  // position q of every face is this thread's own copy: no barrier needed
+      const double* sZ = sZ0 + buf * G * FS + (act ? e : 0) * FS;
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        if (COLOR == 0 || !(shared >> s & 1u)) {
+          const double pn = fma(beta, sFw[s * NQ + q], sZ[s * NQ + q]);
+          sFw[s * NQ + q] = pn;
+          a.pout[off[s]] = pn;
+        }
+      }
+    }
+    __syncthreads();  // staged faces (and their update) visible to the whole CTA
     // colour-0 partials of the shared faces at q: issued now, consumed at the emits
     double prev[6];
     if (COLOR == 1 && on) {
@@ -317,7 +345,7 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
 template <int N, int MODE, int COLOR>
 static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_t t1, cudaStream_t s) {
   using Cf = OpVCfg<N>;
-  const size_t smem = sizeof(double) * (size_t)Cf::smem_doubles();
+  const size_t smem = sizeof(double) * (size_t)Cf::smem_doubles((MODE & 9) == 9);
   auto kern = opV_kernel<N, MODE, COLOR>;
   static int cache[16] = {0};
   int64_t grid = 0;
@@ -383,6 +411,18 @@ static cudaError_t launch_t(hdgb_ctx* c, const double* u, double* r, cudaStream_
   if (layers > g.n3) layers = g.n3;
   const int64_t nslab = (g.n3 + layers - 1) / layers;
   cudaError_t e;
+  if constexpr (!PLAIN && (MODE & 1)) {
+    if (c->pupd_z) {  // transformed PCG: direction update fused into the colour passes (one slab)
+      a.z = c->pupd_z;
+      a.pout = const_cast<double*>(u);
+      const int64_t t1 = g.n3 * per_k;
+      e = c->uniform ? launch_any<N, false, MODE | 8, 0>(c, a, 0, t1, s)
+                     : launch_any<N, false, MODE | 10, 0>(c, a, 0, t1, s);
+      if (e != cudaSuccess) return e;
+      return c->uniform ? launch_any<N, false, MODE | 8, 1>(c, a, 0, t1, s)
+                        : launch_any<N, false, MODE | 10, 1>(c, a, 0, t1, s);
+    }
+  }
   for (int64_t sl = 0; sl <= nslab; ++sl) {
     if (sl < nslab) {
       const int64_t k0 = sl * layers, k1 = k0 + layers < g.n3 ? k0 + layers : g.n3;
