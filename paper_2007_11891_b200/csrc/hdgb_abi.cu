@@ -10,7 +10,6 @@
 
 namespace hdgb {
 cudaError_t launch_cg_init(hdgb_ctx* c, int kind, cudaStream_t s);
-cudaError_t launch_p_update(hdgb_ctx* c, cudaStream_t s, cudaGraphConditionalHandle loop, int has_loop);
 cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* scratch, double* result, cudaStream_t s);
 cudaError_t launch_face_dot(hdgb_ctx* c, const double* x, const double* y, double* scratch, double* result,
                             cudaStream_t s);
