@@ -396,3 +396,36 @@ def test_pinned_host_apply_graph_replay():
         hall[0][:] = u
         dc.apply_host(hall[0], hall[1], variant)
         assert np.array_equal(hall[1], want)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("kind", [0, 1, 2, 3])
+@pytest.mark.parametrize("nonuni", [False, True])
+def test_fused_pcg_every_variant_preconditioner_pair(variant, kind, nonuni):
+    """Every (operator variant, preconditioner) pair of the fused PCG graph (direction update fused
+    into the operator) against the reference PCG algorithm (solver.py:282-321, host loop) driving the
+    same device operator and preconditioner applies."""
+    n, p = (3, 4, 3), 3
+    bc = ("neumann", "dirichlet", "dirichlet", "neumann", "dirichlet", "dirichlet")
+    widths = None
+    if nonuni:
+        rng0 = np.random.default_rng(9)
+        widths = tuple(w / w.sum() for w in (rng0.uniform(0.5, 2.0, k) for k in n))
+    mesh = hb.Mesh(n, (0, 0, 0), (1.0, 1.0, 1.0), bc, widths=widths)
+    ctx = hb.OperatorContext(hb.Basis1D(p, 1.5), mesh, 0.4)
+    dc = hb.device_context(ctx)
+    F = np.random.default_rng(kind + 4 * variant).uniform(-1, 1, dc.n_unknown)
+    Fd = dc.unpack(_dev(F))
+    x = torch.zeros_like(Fd)
+    it, rel, conv = dc.pcg(variant, kind, Fd, x, 1e-10, 0.0, 2000)
+
+    def K(v):
+        return dc.pack(dc.apply(dc.unpack(_dev(v)), variant)).cpu().numpy()
+
+    def P(r):
+        return dc.pack(dc.prec(dc.unpack(_dev(r)), kind)).cpu().numpy()
+
+    xo, ito, relo, convo = O.pcg(K, None if kind == 0 else P, F, np.zeros_like(F))
+    assert conv and convo
+    assert abs(it - ito) <= max(1, int(0.02 * ito)), (it, ito)
+    assert relerr(dc.pack(x).cpu().numpy(), xo) < 1e-8
