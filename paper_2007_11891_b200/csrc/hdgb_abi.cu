@@ -520,6 +520,14 @@ static cudaError_t enqueue_iteration(hdgb_ctx* c, int variant, int prec, cudaGra
   // already): the plain pre-transform, or the transformed colour passes; w = K p with <p, w>
   // and alpha from the operator's last kernel; the x, r update ends the loop once done
   c->pupd_z = v + V_Z * c->vstride;
+  // transformed: folded into the colour passes for 4 <= N <= 11 only; at N = 3 and N >= 13 the
+  // extra staging (z next to p, double the shared memory at N >= 13) measured slower than the
+  // separate pass (44^3 ... 29^3 sweep: p = 2 617 vs 587, p = 12 687 vs 671, p = 16 1032 vs
+  // 845 us/iter)
+  if (variant == HDGB_TRANSFORMED && (c->N < 4 || c->N > 11)) {
+    if ((e = launch_p_update(c, c->s)) != cudaSuccess) return e;
+    c->pupd_z = nullptr;
+  }
   e = launch_op(c, variant, MODE_CG, v + V_P * c->vstride, v + V_W * c->vstride, c->s);
   c->pupd_z = nullptr;
   if (e != cudaSuccess) return e;

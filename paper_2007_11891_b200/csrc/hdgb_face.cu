@@ -470,6 +470,16 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
   }
 }
 
+// ================================================================ CG direction update
+// p = z + beta p (solver.py:320) as its own pass, for the transformed PCG at the degrees where
+// folding it into the colour passes measured slower (hdgb_abi.cu, enqueue_iteration)
+__global__ void p_update_kernel(const double* __restrict__ z, double* __restrict__ p, int64_t n, const CGState* st) {
+  if (st->done) return;
+  const double beta = st->beta;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+}
+
 // ================================================================ generic vectors
 __global__ void __launch_bounds__(HDGB_NT) dot_kernel(const double* __restrict__ x, const double* __restrict__ y,
                                                       int64_t n, double* part, uint32_t* cnt, double* result) {
@@ -956,6 +966,14 @@ cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s, cudaGraphCon
   a.w = v + V_W * c->vstride;
   a.out = v + V_Z * c->vstride;
   return face_any(c, OP_CG_UPDATE, kind, a, s);
+}
+
+cudaError_t launch_p_update(hdgb_ctx* c, cudaStream_t s) {
+  double* v = c->d_vec;
+  const int64_t n = c->n_all;
+  p_update_kernel<<<grid_for(n, 1024), 1024, 0, s>>>(v + V_Z * c->vstride, v + V_P * c->vstride, n, c->d_st);
+  c->launches++;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* scratch, double* result, cudaStream_t s) {

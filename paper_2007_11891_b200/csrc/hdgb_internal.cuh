@@ -325,6 +325,7 @@ cudaError_t launch_prec(hdgb_ctx* c, int kind, const double* in, double* out, cu
 cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s, cudaGraphConditionalHandle loop = 0,
                              int loop_on = 0);
 cudaError_t launch_cg_init(hdgb_ctx* c, int kind, cudaStream_t s);
+cudaError_t launch_p_update(hdgb_ctx* c, cudaStream_t s);
 cudaError_t launch_diag_user(hdgb_ctx* c, const double* diag, const double* in, double* out, cudaStream_t s);
 int grid_for(int64_t work, int per);
 cudaError_t launch_build_tables(hdgb_ctx* c, cudaStream_t s);
