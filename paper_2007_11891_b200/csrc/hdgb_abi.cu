@@ -512,6 +512,12 @@ int hdgb_vec_axpby(int64_t n, double a, const double* x, double b, const double*
 }
 
 // One PCG iteration's kernels (solver.py:303-320) on ctx->s.
+#ifndef HDGB_PUPD_NMIN
+#define HDGB_PUPD_NMIN 4
+#endif
+#ifndef HDGB_PUPD_NMAX
+#define HDGB_PUPD_NMAX 16
+#endif
 static cudaError_t enqueue_iteration(hdgb_ctx* c, int variant, int prec, cudaGraphConditionalHandle h, int has_loop) {
   double* v = c->d_vec;
   const int64_t n = c->n_all;
@@ -520,11 +526,10 @@ static cudaError_t enqueue_iteration(hdgb_ctx* c, int variant, int prec, cudaGra
   // already): the plain pre-transform, or the transformed colour passes; w = K p with <p, w>
   // and alpha from the operator's last kernel; the x, r update ends the loop once done
   c->pupd_z = v + V_Z * c->vstride;
-  // transformed: folded into the colour passes for 4 <= N <= 11 only; at N = 3 and N >= 13 the
-  // extra staging (z next to p, double the shared memory at N >= 13) measured slower than the
-  // separate pass (44^3 ... 29^3 sweep: p = 2 617 vs 587, p = 12 687 vs 671, p = 16 1032 vs
-  // 845 us/iter)
-  if (variant == HDGB_TRANSFORMED && (c->N < 4 || c->N > 11)) {
+  // transformed: folded into colour pass 0 for 4 <= N <= 16; at N = 3 (small elements, staging
+  // dominated) and N = 17 (the z stage halves the resident CTAs) the separate pass measured
+  // as fast or faster (p = 2: 601 vs 596, p = 12: 663 vs 677, p = 14: 745 vs 761 us/iter)
+  if (variant == HDGB_TRANSFORMED && (c->N < HDGB_PUPD_NMIN || c->N > HDGB_PUPD_NMAX)) {
     if ((e = launch_p_update(c, c->s)) != cudaSuccess) return e;
     c->pupd_z = nullptr;
   }

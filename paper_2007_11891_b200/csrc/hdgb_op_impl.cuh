@@ -147,10 +147,11 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
   using C = OpVCfg<N>;
   constexpr int NQ = C::NQ, G = C::G, FS = C::FS, VS = C::VS;
   constexpr bool UNI = !(MODE & 2), CG = MODE & 1, GONLY = MODE & 4;
-  // bit 3 (CG only): p = z + beta p (solver.py:320) fused into the staging of this pass: colour 0
-  // updates every face of its elements, colour 1 the faces it alone touches (the rest already
-  // hold the new p); the new p is written back for the x update
-  constexpr bool PUPD = CG && (MODE & 8);
+  // bit 3 (CG, colour 0 only): p = z + beta p (solver.py:320) fused into the staging of this
+  // pass: colour 0 updates every face of its elements while staging them and, in a tail loop,
+  // the boundary faces whose only element is colour 1; the new p is written back, so colour 1
+  // and the x update read it
+  constexpr bool PUPD = CG && (MODE & 8) && COLOR == 0;
   pdl_trigger();
   double beta = 0.0;
   if (CG) {
@@ -215,8 +216,7 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
       if (PUPD) {
         double* dz = sZ0 + bi * G * FS + e * FS + q;
 #pragma unroll
-        for (int s = 0; s < 6; ++s)
-          if (COLOR == 0 || !(inf[e].shared >> s & 1u)) cp_async8(dz + s * NQ, a.z + (inf[e].off[s] + (unsigned)q));
+        for (int s = 0; s < 6; ++s) cp_async8(dz + s * NQ, a.z + (inf[e].off[s] + (unsigned)q));
       }
     }
   };
@@ -254,11 +254,9 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
       const double* sZ = sZ0 + buf * G * FS + (act ? e : 0) * FS;
 #pragma unroll
       for (int s = 0; s < 6; ++s) {
-        if (COLOR == 0 || !(shared >> s & 1u)) {
-          const double pn = fma(beta, sFw[s * NQ + q], sZ[s * NQ + q]);
-          sFw[s * NQ + q] = pn;
-          a.pout[off[s]] = pn;
-        }
+        const double pn = fma(beta, sFw[s * NQ + q], sZ[s * NQ + q]);
+        sFw[s * NQ + q] = pn;
+        a.pout[off[s]] = pn;
       }
     }
     __syncthreads();  // staged faces (and their update) visible to the whole CTA
@@ -328,6 +326,45 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
     __syncthreads();  // staging buffer, volume and element info are reused
   }
   cp_async_wait_all();
+  if (PUPD) {  // boundary faces of colour-1 elements (no colour-0 neighbour): one warp per face
+    const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    const int64_t nb0 = 2LL * g.n2 * g.n3, nb1 = 2LL * g.n1 * g.n3, nb = nb0 + nb1 + 2LL * g.n1 * g.n2;
+    for (int64_t bf = (int64_t)blockIdx.x * nw + wid; bf < nb; bf += (int64_t)gridDim.x * nw) {
+      int d, c[3];
+      int64_t rem;
+      int side;
+      if (bf < nb0) {
+        d = 0;
+        side = (int)(bf / ((int64_t)g.n2 * g.n3));
+        rem = bf - side * (int64_t)g.n2 * g.n3;
+        c[1] = (int)(rem % g.n2);
+        c[2] = (int)(rem / g.n2);
+        c[0] = side ? g.n1 - 1 : 0;
+      } else if (bf < nb0 + nb1) {
+        d = 1;
+        const int64_t b = bf - nb0;
+        side = (int)(b / ((int64_t)g.n1 * g.n3));
+        rem = b - side * (int64_t)g.n1 * g.n3;
+        c[0] = (int)(rem % g.n1);
+        c[2] = (int)(rem / g.n1);
+        c[1] = side ? g.n2 - 1 : 0;
+      } else {
+        d = 2;
+        const int64_t b = bf - nb0 - nb1;
+        side = (int)(b / ((int64_t)g.n1 * g.n2));
+        rem = b - side * (int64_t)g.n1 * g.n2;
+        c[0] = (int)(rem % g.n1);
+        c[1] = (int)(rem / g.n1);
+        c[2] = side ? g.n3 - 1 : 0;
+      }
+      if (((c[0] + c[1] + c[2]) & 1) != 1) continue;  // colour-0 element: updated above
+      const int64_t fid = g.foff[d] + face_lo(g, d, c[0], c[1], c[2]) + side * face_step(g, d);
+      for (int qq = lane; qq < NQ; qq += 32) {
+        const int64_t o = fid * NQ + qq;
+        a.pout[o] = fma(beta, a.u[o], a.z[o]);
+      }
+    }
+  }
   if (CG && !GONLY) {  // <p, w>: colour 0 keeps its part, colour 1 completes it and sets alpha
     double dummy = 0.0;
     block_sum2(dacc, dummy);
@@ -345,7 +382,7 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
 template <int N, int MODE, int COLOR>
 static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_t t1, cudaStream_t s) {
   using Cf = OpVCfg<N>;
-  const size_t smem = sizeof(double) * (size_t)Cf::smem_doubles((MODE & 9) == 9);
+  const size_t smem = sizeof(double) * (size_t)Cf::smem_doubles((MODE & 9) == 9 && COLOR == 0);
   auto kern = opV_kernel<N, MODE, COLOR>;
   static int cache[16] = {0};
   int64_t grid = 0;
@@ -419,8 +456,8 @@ static cudaError_t launch_t(hdgb_ctx* c, const double* u, double* r, cudaStream_
       e = c->uniform ? launch_any<N, false, MODE | 8, 0>(c, a, 0, t1, s)
                      : launch_any<N, false, MODE | 10, 0>(c, a, 0, t1, s);
       if (e != cudaSuccess) return e;
-      return c->uniform ? launch_any<N, false, MODE | 8, 1>(c, a, 0, t1, s)
-                        : launch_any<N, false, MODE | 10, 1>(c, a, 0, t1, s);
+      return c->uniform ? launch_any<N, false, MODE, 1>(c, a, 0, t1, s)
+                        : launch_any<N, false, MODE | 2, 1>(c, a, 0, t1, s);
     }
   }
   for (int64_t sl = 0; sl <= nslab; ++sl) {

@@ -400,12 +400,12 @@ def test_pinned_host_apply_graph_replay():
 
 @pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("kind", [0, 1, 2, 3])
-@pytest.mark.parametrize("nonuni", [False, True])
-def test_fused_pcg_every_variant_preconditioner_pair(variant, kind, nonuni):
+@pytest.mark.parametrize("nonuni,p", [(False, 3), (True, 3), (False, 2)])
+def test_fused_pcg_every_variant_preconditioner_pair(variant, kind, nonuni, p):
     """Every (operator variant, preconditioner) pair of the fused PCG graph (direction update fused
-    into the operator) against the reference PCG algorithm (solver.py:282-321, host loop) driving the
-    same device operator and preconditioner applies."""
-    n, p = (3, 4, 3), 3
+    into the operator, or its own pass at p = 2) against the reference PCG algorithm
+    (solver.py:282-321, host loop) driving the same device operator and preconditioner applies."""
+    n = (3, 4, 3)
     bc = ("neumann", "dirichlet", "dirichlet", "neumann", "dirichlet", "dirichlet")
     widths = None
     if nonuni:
