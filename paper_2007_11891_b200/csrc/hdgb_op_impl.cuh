@@ -106,7 +106,24 @@ struct OpVCfg {
   // register budget (CTAs per SM): measured on the config-3 sweep (p = 2..16)
   static constexpr int MINB = NT > 256 ? 2 : (N <= 7 ? 3 : (N <= 11 ? 2 : 3));
 #endif
-  static constexpr int FS = 6 * NQ;                     // staged faces of one element
+  // staging of the six faces: bulk async copies (TMA unit, one mbarrier per buffer) for
+  // N >= HDGB_OPV_TMA_NMIN, per-thread cp.async below.  A face of odd NQ starts on an 8-byte
+  // boundary every other face: its 16-byte aligned cover (NQ + 1 doubles) is copied into a slot
+  // of NQ + 1 doubles and read at offset (face offset & 1).  Measured on the config-3 sweep:
+  // the per-face bulk copies (6 per element, 72 B - 2.3 KB each) are slower than cp.async up to
+  // p = 8 (transformed apply p = 3 347 vs 181 us, p = 8 290 vs 259 us: the copy engine's
+  // per-request cost), equal at p = 12 and 16, and faster for the fused transformed PCG at
+  // p = 12 (632 vs 657 us/iter), slightly slower again at p = 16 (plain 731 vs 715 us), so
+  // 13 <= N <= 16 use them.
+#ifndef HDGB_OPV_TMA_NMIN
+#define HDGB_OPV_TMA_NMIN 13
+#endif
+#ifndef HDGB_OPV_TMA_NMAX
+#define HDGB_OPV_TMA_NMAX 16
+#endif
+  static constexpr bool TMA = N >= HDGB_OPV_TMA_NMIN && N <= HDGB_OPV_TMA_NMAX;
+  static constexpr int FSTR = (TMA && (NQ & 1)) ? NQ + 1 : NQ;  // face slot stride
+  static constexpr int FS = 6 * FSTR;                   // staged faces of one element
   static constexpr int VS = N * NQ;                     // U volume of one element
   // dz_inv lines in registers (N values per thread) up to N = 11; from a shared copy of the
   // table for N >= 12, where the registers are worth more (measured: p = 12 339 -> 312 us,
@@ -117,8 +134,10 @@ struct OpVCfg {
   static constexpr bool DZS = N >= 12;
 #endif
   // PUPD (transformed PCG, direction update fused into colour pass 0): z staged next to p
+  // z staging (PUPD) starts 16-byte aligned after the volume and the dz_inv copy
+  static constexpr int ZOFF = (G * (2 * FS + VS) + (DZS ? N * NQ : 0) + 1) / 2 * 2;
   __host__ __device__ static constexpr int smem_doubles(bool pupd = false) {
-    return G * (2 * FS + VS) + (DZS ? N * NQ : 0) + (pupd ? 2 * G * FS : 0);
+    return pupd ? ZOFF + 2 * G * FS : G * (2 * FS + VS) + (DZS ? N * NQ : 0);
   }
 };
 
@@ -159,8 +178,11 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
     if (a.st->done) return;
     if (PUPD) beta = a.st->beta;
   }
+  constexpr bool TMA = C::TMA;
+  constexpr int FSTR = C::FSTR;
   extern __shared__ __align__(16) double smem[];
-  double* sF0 = smem;              // 2 x G x [6][NQ] staged faces
+  __shared__ __align__(8) uint64_t sBar[2];  // TMA: one transaction barrier per staging buffer
+  double* sF0 = smem;              // 2 x G x [6][FSTR] staged faces
   double* sU = smem + 2 * G * FS;  // G x [N][NQ] volume
   __shared__ ElemInfo sInfo[2][G];
   const Geo& g = a.g;
@@ -207,8 +229,40 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
       }
     }
   };
-  double* sZ0 = smem + G * (2 * FS + VS) + (C::DZS ? N * NQ : 0);  // PUPD: 2 x G x [6][NQ] staged z
+  double* sZ0 = smem + C::ZOFF;  // PUPD: 2 x G x [6][FSTR] staged z
+  if (TMA && tid == 0) {
+    mbar_init(&sBar[0], 1);
+    mbar_init(&sBar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // TMA: warp 0 stages the group (lane 0 arms the barrier with the byte count, the lanes issue
+  // one face copy each); the previous generic accesses of the buffer were fenced by the loop's
+  // closing barrier, ordered before the async writes by fence.proxy.async
+  auto stage_tma = [&](const ElemInfo* inf, double* buf, int bi) {
+    if (tid >= 32) return;
+    constexpr uint32_t CNT = (NQ & 1) ? NQ + 1 : NQ;  // doubles per face copy (even)
+    constexpr int NC = PUPD ? 12 : 6;
+    if (tid == 0) {
+      uint32_t nval = 0;
+      for (int ee = 0; ee < G; ++ee) nval += inf[ee].valid ? 1u : 0u;
+      fence_proxy_async();
+      mbar_expect_tx(&sBar[bi], nval * NC * CNT * 8u);
+    }
+    __syncwarp();
+    for (int c = tid; c < G * NC; c += 32) {
+      const int ee = c / NC, k = c - ee * NC, sface = k % 6;
+      if (!inf[ee].valid) continue;
+      const unsigned off = inf[ee].off[sface];
+      const unsigned lo = (NQ & 1) ? (off & ~1u) : off;
+      double* dst = (k < 6 ? buf : sZ0 + bi * G * FS) + ee * FS + sface * FSTR;
+      bulk_g2s(dst, (k < 6 ? a.u : a.z) + lo, CNT * 8u, &sBar[bi]);
+    }
+  };
   auto stage = [&](const ElemInfo* inf, double* buf, int bi) {
+    if (TMA) {
+      stage_tma(inf, buf, bi);
+      return;
+    }
     if (act && inf[e].valid) {
       double* dst = buf + e * FS + q;
 #pragma unroll
@@ -228,13 +282,14 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
   if (!CG) pdl_wait();  // u and r come from earlier kernels
   if (gi < ngroups) stage(sInfo[0], sF0, 0);
   cp_async_commit();
-  for (int buf = 0; gi < ngroups; gi += gridDim.x, buf ^= 1) {
+  for (int buf = 0, k = 0; gi < ngroups; gi += gridDim.x, buf ^= 1, ++k) {
     const int64_t gn = gi + gridDim.x;
     if (gn < ngroups) info(gn, sInfo[buf ^ 1]);
     __syncthreads();
     if (gn < ngroups) stage(sInfo[buf ^ 1], sF0 + (buf ^ 1) * G * FS, buf ^ 1);
     cp_async_commit();
-    asm volatile("cp.async.wait_group 1;\n" ::);
+    if (TMA) mbar_wait(&sBar[buf], (uint32_t)(k >> 1) & 1u);
+    else asm volatile("cp.async.wait_group 1;\n" ::);
     // element geometry into registers once (sInfo[buf] was published a barrier ago)
     const ElemInfo& I = sInfo[buf][act ? e : 0];
     const bool on = act && I.valid;
@@ -248,14 +303,18 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
     const unsigned shared = I.shared;
     const double al0 = I.al[0], al1 = I.al[1], al2 = I.al[2], al3 = I.al[3];
     double* sFw = sF0 + buf * G * FS + (act ? e : 0) * FS;
-    const double* sF = sFw;
+    double* fb[6];  // face s of the element: fb[s][position]
+#pragma unroll
+    for (int s2 = 0; s2 < 6; ++s2) fb[s2] = sFw + s2 * FSTR + ((TMA && (NQ & 1)) ? (I.off[s2] & 1u) : 0u);
     double* vU = sU + (act ? e : 0) * VS;
-    if (PUPD && on) {  // position q of every face is this thread's own copy: no barrier needed
+    if (PUPD && on) {  // position q of every face is this thread's own copy (cp.async) or
+                       // complete for every thread (TMA barrier): no extra CTA barrier needed
       const double* sZ = sZ0 + buf * G * FS + (act ? e : 0) * FS;
 #pragma unroll
       for (int s = 0; s < 6; ++s) {
-        const double pn = fma(beta, sFw[s * NQ + q], sZ[s * NQ + q]);
-        sFw[s * NQ + q] = pn;
+        double* fp = fb[s] + q;
+        const double pn = fma(beta, *fp, sZ[(fb[s] - sFw) + q]);
+        *fp = pn;
         a.pout[off[s]] = pn;
       }
     }
@@ -279,15 +338,15 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
       a.r[off[s]] = val;
     };
     if (on) {  // phase 1: x-line of (a2, a3) = (qa, qb)
-      const double xr0 = sF[q], xr1 = sF[NQ + q];
+      const double xr0 = fb[0][q], xr1 = fb[1][q];
       const double x0 = al1 * xr0, x1 = al1 * xr1;
       const double by0 = al2 * b0a, by1 = al2 * b1a, bz0 = al3 * b0b, bz1 = al3 * b1b;
       const double base = UNI ? 0.0 : a.lam * al0 + al2 * lama + al3 * lamb;
       double ax0 = 0.0, ax1 = 0.0;
 #pragma unroll
       for (int a1 = 0; a1 < N; ++a1) {
-        const double y0 = sF[2 * NQ + a1 * N + qb], y1 = sF[3 * NQ + a1 * N + qb];
-        const double z0 = sF[4 * NQ + a1 * N + qa], z1 = sF[5 * NQ + a1 * N + qa];
+        const double y0 = fb[2][a1 * N + qb], y1 = fb[3][a1 * N + qb];
+        const double z0 = fb[4][a1 * N + qa], z1 = fb[5][a1 * N + qa];
         double F = K.B0[a1] * x0;
         F = fma(K.B1[a1], x1, F);
         F = fma(by0, y0, F);
@@ -317,7 +376,7 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
         az0 = fma(K.B0[k], vz, az0);
         az1 = fma(K.B1[k], vz, az1);
       }
-      const double yr0 = sF[2 * NQ + q], yr1 = sF[3 * NQ + q], zr0 = sF[4 * NQ + q], zr1 = sF[5 * NQ + q];
+      const double yr0 = fb[2][q], yr1 = fb[3][q], zr0 = fb[4][q], zr1 = fb[5][q];
       emit(2, al2 * ay0, al2 * yr0, yr0);
       emit(3, al2 * ay1, al2 * yr1, yr1);
       emit(4, al3 * az0, al3 * zr0, zr0);

@@ -400,7 +400,7 @@ def test_pinned_host_apply_graph_replay():
 
 @pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("kind", [0, 1, 2, 3])
-@pytest.mark.parametrize("nonuni,p", [(False, 3), (True, 3), (False, 2)])
+@pytest.mark.parametrize("nonuni,p", [(False, 3), (True, 3), (False, 2), (True, 12)])
 def test_fused_pcg_every_variant_preconditioner_pair(variant, kind, nonuni, p):
     """Every (operator variant, preconditioner) pair of the fused PCG graph (direction update fused
     into the operator, or its own pass at p = 2) against the reference PCG algorithm
