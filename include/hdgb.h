@@ -14,6 +14,13 @@
  * (see INTEGRATION.md).  No exceptions cross the ABI: every call returns an
  * hdgb_status; hdgb_last_error() gives the message of the last failure on the
  * calling thread.
+ *
+ * Concurrency: hdgb_op_apply(HDGB_TRANSFORMED), hdgb_prec_apply and
+ * hdgb_face_transform only read the context and may run concurrently on
+ * different streams.  hdgb_op_apply(HDGB_PLAIN) (eigen-space intermediate),
+ * the host-buffer applies, the pre/post entry points and hdgb_pcg use the
+ * context's scratch: keep them in order on one stream per context, or use one
+ * context per concurrent solver.
  */
 #ifndef HDGB_H
 #define HDGB_H
