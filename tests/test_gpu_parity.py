@@ -429,3 +429,29 @@ def test_fused_pcg_every_variant_preconditioner_pair(variant, kind, nonuni, p):
     assert conv and convo
     assert abs(it - ito) <= max(1, int(0.02 * ito)), (it, ito)
     assert relerr(dc.pack(x).cpu().numpy(), xo) < 1e-8
+
+
+@pytest.mark.parametrize("p,m", [(8, 44), (16, 29), (2, 91), (8, 128)])
+def test_full_size_operator_properties(p, m):
+    """BASELINE config 3 (2e7 unknowns) and config 5 (128^3, 5e8 unknowns) at full size, through the
+    size-independent properties of K: symmetry on the unknown faces, linearity,
+    bitwise determinism, for both operator variants."""
+    mesh = hb.Mesh((m, m, m))
+    ctx = hb.make_context(mesh, p, hb.SolverConfig(lam=1.0))
+    dc = hb.device_context(ctx)
+    gen = torch.Generator(device="cuda").manual_seed(p * 1000 + m)
+    x = torch.rand(mesh.n_all(p), dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    y = torch.rand(mesh.n_all(p), dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    dc.zero_dirichlet(x)
+    dc.zero_dirichlet(y)
+    for variant in (0, 1):
+        kx, ky = dc.apply(x, variant), dc.apply(y, variant)
+        asym = abs(float(torch.dot(x, ky) - torch.dot(y, kx)))
+        assert asym <= 1e-12 * float(torch.linalg.norm(x) * torch.linalg.norm(ky)), (variant, asym)
+        kxy = dc.apply(0.75 * x - 1.25 * y, variant)
+        lin = float(torch.max(torch.abs(kxy - (0.75 * kx - 1.25 * ky))))
+        assert lin <= 1e-12 * float(torch.max(torch.abs(kx)) + torch.max(torch.abs(ky))), (variant, lin)
+        assert torch.equal(dc.apply(x, variant), kx)
+        del kx, ky, kxy
+    del dc, ctx, x, y
+    torch.cuda.empty_cache()
