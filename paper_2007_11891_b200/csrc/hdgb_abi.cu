@@ -533,10 +533,14 @@ static cudaError_t enqueue_iteration(hdgb_ctx* c, int variant, int prec, cudaGra
     if ((e = launch_p_update(c, c->s)) != cudaSuccess) return e;
     c->pupd_z = nullptr;
   }
+  // block PCG: x += alpha p deferred into the next pre-transform (which stages p anyway), the
+  // r update and ||r|| into the preconditioner kernel: no separate x/r pass (x_final after the loop)
+  c->pupd_x = (variant == HDGB_PLAIN && prec == HDGB_PREC_BLOCK) ? v + V_X * c->vstride : nullptr;
   e = launch_op(c, variant, MODE_CG, v + V_P * c->vstride, v + V_W * c->vstride, c->s);
   c->pupd_z = nullptr;
-  if (e != cudaSuccess) return e;
-  return launch_cg_update(c, prec, c->s, h, has_loop);  // x,r update; z = P r; ||r||, <r,z>
+  if (e == cudaSuccess) e = launch_cg_update(c, prec, c->s, h, has_loop);  // x,r update; z = P r; ||r||, <r,z>
+  c->pupd_x = nullptr;
+  return e;
 }
 
 // Build (once per variant/prec) a graph whose conditional WHILE node runs PCG iterations
@@ -636,6 +640,7 @@ int hdgb_pcg(hdgb_ctx* c, int variant, int prec, const double* F, double* x, dou
         if (h->done) break;
       }
     }
+    if (variant == HDGB_PLAIN && prec == HDGB_PREC_BLOCK) HDGB_CUDA(launch_x_final(c, c->s));  // last deferred x update
     HDGB_CUDA(cudaMemcpyAsync(h, c->d_st, sizeof(CGState), cudaMemcpyDeviceToHost, c->s));
     HDGB_CUDA(cudaStreamSynchronize(c->s));
     if (use_graph) c->launches += c->graph_launches[variant][prec] * (int64_t)(h->it > 0 ? h->it : 1);

@@ -174,9 +174,14 @@ struct FxCfg {
   // 446 -> 420 us with 3 CTAs/SM); larger N prefetch u into registers (p = 12/16 faster)
   // (inside the PCG, CG = 1, the register-prefetch variant measured faster: 941 -> 886 us/iter)
 #ifdef HDGB_FX_POST_TMA
-  static constexpr int OPS = ((FK == FX_POST && HDGB_FX_POST_TMA) || (FK == FX_TRANSFORM && CG)) ? 2 : 1;
+  static constexpr int OPS = (FK == FX_TRANSFORM && CG == 2) ? 3
+                             : ((FK == FX_POST && HDGB_FX_POST_TMA) || (FK == FX_TRANSFORM && CG) || (FK == FX_UPDATE && CG)) ? 2
+                                                                                                               : 1;
 #else
-  static constexpr int OPS = ((FK == FX_POST && !CG && N <= 11) || (FK == FX_TRANSFORM && CG)) ? 2 : 1;
+  // staged operands: FX_TRANSFORM CG = 1: z, p; CG = 2: z, p, x; FX_UPDATE CG = 1: r, w
+  static constexpr int OPS = (FK == FX_TRANSFORM && CG == 2) ? 3
+                             : ((FK == FX_POST && !CG && N <= 11) || (FK == FX_TRANSFORM && CG) || (FK == FX_UPDATE && CG)) ? 2
+                                                                                                                  : 1;
 #endif
   static constexpr bool BLOCK = FK == FX_PREC || FK == FX_INIT || FK == FX_UPDATE;
   // per-group slice, 128-byte aligned (bulk-copy destinations need 16)
@@ -229,21 +234,30 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
   using C = FxCfg<N, FK, CG>;
   constexpr int N2 = C::N2, FPW = C::FPW, NP = C::NP, WP = C::WP, BATW = C::BATW, S = C::S, GT = C::GT;
   constexpr int GW = C::GW, EPT = C::EPT, OPS = C::OPS;
-  constexpr bool UTMA = OPS == 2;
+  constexpr bool UTMA = OPS >= 2;
   constexpr bool BLOCK = C::BLOCK;
   constexpr bool RED = FK == FX_INIT || FK == FX_UPDATE;
   constexpr bool POST = FK == FX_POST;
   // plain PCG: the direction update p = z + beta p (solver.py:320) fused into the
   // pre-transform of the next operator apply: stages z and p, writes p and (T (x) T) p
   constexpr bool PUPD = FK == FX_TRANSFORM && CG;
+  // block PCG: the deferred x += alpha_prev p_prev rides along (CG = 2: x staged as well; the
+  // last one is applied after the loop), and the r -= alpha w update with ||r|| moves into the
+  // preconditioner kernel (FX_UPDATE, CG = 1: r and w staged), which then decides convergence
+  constexpr bool XUPD = FK == FX_TRANSFORM && CG == 2;
+  constexpr bool RUPD = FK == FX_UPDATE && CG;
   constexpr bool ODD = N & 1;  // row-wise stores N doubles apart are bank-conflict-free
   constexpr bool EARLY = RED || (POST && CG) || PUPD;  // reads the PCG state first
   pdl_trigger();
   if (EARLY) {
     pdl_wait();
-    if (a.st->done) return;
+    if (a.st->done) {
+      if (RUPD && a.loop_on && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(a.loop, 0u);
+      return;
+    }
   }
   const double beta = PUPD ? a.st->beta : 0.0;
+  const double alpha = (XUPD || RUPD) ? a.st->alpha : 0.0;
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t sBar[C::NG][S];
   __shared__ double sWq[N];  // FX_POST: quadrature weights (dynamic index: keep out of the constant bank)
@@ -272,7 +286,8 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
   };
   // FX_POST overwrites G (a.out) in place with r; each batch is staged before it is written
   const double* src = POST ? a.out : a.in;
-  const double* src2 = POST ? a.in : a.p;  // second staged operand (UTMA): u, or p
+  const double* src2 = POST ? a.in : (RUPD ? a.w : a.p);  // second staged operand: u, w or p
+  const double* src3 = a.x;                                // third (XUPD): x
   const int64_t nbat = (a.nfaces + FPW - 1) / FPW;
   const int64_t gg = (int64_t)blockIdx.x * C::NG + grp, ngg = (int64_t)gridDim.x * C::NG;
   const int64_t nmine = gg < nbat ? (nbat - 1 - gg) / ngg + 1 : 0;
@@ -288,14 +303,16 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
     if (bulk != total) {
       dst[bulk] = src[lo + bulk];
       if (UTMA) dst[BATW + bulk] = src2[lo + bulk];
+      if (OPS == 3) dst[2 * BATW + bulk] = src3[lo + bulk];
     }
     mbar_expect_tx(bar, bulk * 8u * OPS);
     bulk_g2s(dst, src + lo, bulk * 8u, bar);
     if (UTMA) bulk_g2s(dst + BATW, src2 + lo, bulk * 8u, bar);
+    if (OPS == 3) bulk_g2s(dst + 2 * BATW, src3 + lo, bulk * 8u, bar);
   };
   if (gl == 0)
     for (int64_t k = 0; k < S - 1 && k < nmine; ++k) issue(k);
-  double rz = 0.0;
+  double rz = 0.0, rr = 0.0;
   for (int64_t k = 0; k < nmine; ++k) {
     if (gl == 0 && k + S - 1 < nmine) {
       fence_proxy_async();  // the stage's previous generic accesses happen before the refill
@@ -321,10 +338,24 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
       const double* xs = sX + f * N2 + l;
       if (PUPD) {  // p = z + beta p on column l, kept in the p stage for the epilogue store
         double* ps = sX + BATW + f * N2 + l;
+        double* xx = sX + 2 * BATW + f * N2 + l;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-          x[i] = fma(beta, ps[i * N], xs[i * N]);
+          const double po = ps[i * N];
+          x[i] = fma(beta, po, xs[i * N]);
           ps[i * N] = x[i];
+          if (XUPD) xx[i * N] = fma(alpha, po, xx[i * N]);  // x += alpha_prev p_prev (solver.py:313)
+        }
+      } else if (RUPD) {  // r -= alpha w (solver.py:314), kept in the w stage for the epilogue
+        double* ws = sX + BATW + f * N2 + l;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          x[i] = fma(-alpha, ws[i * N], xs[i * N]);
+          ws[i * N] = x[i];
+        }
+        if (kind_counts(finfo_kind(inf))) {
+#pragma unroll
+          for (int i = 0; i < N; ++i) rr = fma(x[i], x[i], rr);
         }
       } else {
 #pragma unroll
@@ -413,6 +444,8 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
       a.out[gi] = v;
       if (FK == FX_INIT) a.p[gi] = v;
       if (PUPD) a.p[gi] = sX[BATW + it];
+      if (XUPD) a.x[gi] = sX[2 * BATW + it];
+      if (RUPD) a.r[gi] = sX[BATW + it];
     }
     gsync();  // the stage and the tile are reused
   }
@@ -426,17 +459,34 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
     }
   }
   if (RED) {
-    double dummy = 0.0;
-    block_sum2(rz, dummy);
-    if (publish_last(a.part, rz, 0.0, &a.st->cnt[3])) {
-      double trz, t0;
-      final_sum2(a.part, gridDim.x, trz, t0);
+    block_sum2(rz, rr);
+    if (publish_last(a.part, rz, rr, &a.st->cnt[3])) {
+      double trz, trr;
+      final_sum2(a.part, gridDim.x, trz, trr);
       if (threadIdx.x == 0) {
-        if (FK == FX_INIT) cg_init_z(a.st, trz);
-        else cg_update_z(a.st, trz);
+        CGState* st = a.st;
+        if (FK == FX_INIT) {
+          cg_init_z(st, trz);
+        } else if (RUPD) {  // ||r|| -> convergence (solver.py:315-318), then beta
+          cg_update_r(st, trr);
+          if (!st->done) cg_update_z(st, trz);
+          if (a.loop_on && st->done) cudaGraphSetConditional(a.loop, 0u);
+        } else {
+          cg_update_z(st, trz);
+        }
       }
     }
   }
+}
+
+// ================================================================ deferred x update
+// block PCG: the last x += alpha p after the loop (every exit but a breakdown or a non-finite
+// residual follows an r update whose x update is still pending)
+__global__ void x_final_kernel(double* __restrict__ x, const double* __restrict__ p, int64_t n, const CGState* st) {
+  if (st->status != HDGB_OK || st->it == 0) return;
+  const double alpha = st->alpha;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = fma(alpha, p[i], x[i]);
 }
 
 // ================================================================ CG direction update
@@ -833,6 +883,13 @@ static cudaError_t face_n(hdgb_ctx* c, int op, int prec, const FaceArgs& a, cuda
       }
       return cudaSuccess;
     case OP_CG_UPDATE:
+      if (prec == HDGB_PREC_BLOCK && c->pupd_x) {  // r update, ||r||, z = P r, <r,z> in one kernel
+        FaceArgs b = a;
+        b.in = a.r;
+        TabOff to;
+        to.set(N);
+        return fx_launch<N, FX_UPDATE, 1>(c, b, c->h_tab.data() + to.St, c->h_tab.data() + to.S, N * N, s);
+      }
       if ((e = pw_prec<N, PW_UPDATE, true>(c, prec, a, s)) != cudaSuccess) return e;
       if (prec == HDGB_PREC_BLOCK) {
         FaceArgs b = a;
@@ -864,10 +921,12 @@ cudaError_t launch_face_transform_pupd(hdgb_ctx* c, const double* A_host, const 
   a.in = z;
   a.p = p;
   a.out = out;
+  a.x = c->pupd_x;  // block PCG: deferred x update rides along
   switch (c->N) {
 #define HDGB_CASE(n) \
   case n:            \
-    return fx_launch<n, FX_TRANSFORM, 1>(c, a, A_host, nullptr, 0, s);
+    return a.x ? fx_launch<n, FX_TRANSFORM, 2>(c, a, A_host, nullptr, 0, s) \
+               : fx_launch<n, FX_TRANSFORM, 1>(c, a, A_host, nullptr, 0, s);
     HDGB_CASE(2) HDGB_CASE(3) HDGB_CASE(4) HDGB_CASE(5) HDGB_CASE(6) HDGB_CASE(7) HDGB_CASE(8) HDGB_CASE(9)
     HDGB_CASE(10) HDGB_CASE(11) HDGB_CASE(12) HDGB_CASE(13) HDGB_CASE(14) HDGB_CASE(15) HDGB_CASE(16)
     HDGB_CASE(17)
@@ -935,6 +994,14 @@ cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s, cudaGraphCon
   a.w = v + V_W * c->vstride;
   a.out = v + V_Z * c->vstride;
   return face_any(c, OP_CG_UPDATE, kind, a, s);
+}
+
+cudaError_t launch_x_final(hdgb_ctx* c, cudaStream_t s) {
+  double* v = c->d_vec;
+  const int64_t n = c->n_all;
+  x_final_kernel<<<grid_for(n, 1024), 1024, 0, s>>>(v + V_X * c->vstride, v + V_P * c->vstride, n, c->d_st);
+  c->launches++;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_p_update(hdgb_ctx* c, cudaStream_t s) {

@@ -228,6 +228,7 @@ __device__ __forceinline__ void cg_init_z(CGState* st, double rz) {
   st->rho = rz;
   st->rz = rz;
   st->beta = 0.0;
+  st->alpha = 0.0;  // the deferred x update of the first iteration adds 0 * p
 }
 __device__ __forceinline__ void cg_update_r(CGState* st, double rr) {  // after x += a p, r -= a w
   const double rn = sqrt(rr);
@@ -288,6 +289,7 @@ struct hdgb_ctx {
   // plain PCG: z slot of the direction update fused into the pre-transform (set around
   // the operator launch of an iteration; null otherwise)
   const double* pupd_z = nullptr;
+  double* pupd_x = nullptr;  // block PCG: x slot of the deferred x update (also selects the fused r update)
   double* d_io = nullptr;         // host-path staging (2 * n_all)
   cudaStream_t s = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -326,6 +328,7 @@ cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s, cudaGraphCon
                              int loop_on = 0);
 cudaError_t launch_cg_init(hdgb_ctx* c, int kind, cudaStream_t s);
 cudaError_t launch_p_update(hdgb_ctx* c, cudaStream_t s);
+cudaError_t launch_x_final(hdgb_ctx* c, cudaStream_t s);
 cudaError_t launch_diag_user(hdgb_ctx* c, const double* diag, const double* in, double* out, cudaStream_t s);
 int grid_for(int64_t work, int per);
 cudaError_t launch_build_tables(hdgb_ctx* c, cudaStream_t s);
