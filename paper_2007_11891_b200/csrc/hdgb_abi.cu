@@ -530,12 +530,13 @@ static cudaError_t enqueue_iteration(hdgb_ctx* c, int variant, int prec, cudaGra
   // dominated) and N = 17 (the z stage halves the resident CTAs) the separate pass measured
   // as fast or faster (p = 2: 601 vs 596, p = 12: 663 vs 677, p = 14: 745 vs 761 us/iter)
   if (variant == HDGB_TRANSFORMED && (c->N < HDGB_PUPD_NMIN || c->N > HDGB_PUPD_NMAX)) {
-    if ((e = launch_p_update(c, c->s)) != cudaSuccess) return e;
+    if ((e = launch_p_update(c, c->s)) != cudaSuccess) return e;  // p and the deferred x
     c->pupd_z = nullptr;
   }
-  // block PCG: x += alpha p deferred into the next pre-transform (which stages p anyway), the
-  // r update and ||r|| into the preconditioner kernel: no separate x/r pass (x_final after the loop)
-  c->pupd_x = (variant == HDGB_PLAIN && prec == HDGB_PREC_BLOCK) ? v + V_X * c->vstride : nullptr;
+  // x += alpha p (solver.py:313) deferred into the next direction update, which reads p anyway
+  // (x_final applies the last one after the loop); the block preconditioner kernel also takes
+  // over r -= alpha w and ||r||, the other preconditioners' update pass only updates r
+  c->pupd_x = v + V_X * c->vstride;
   e = launch_op(c, variant, MODE_CG, v + V_P * c->vstride, v + V_W * c->vstride, c->s);
   c->pupd_z = nullptr;
   if (e == cudaSuccess) e = launch_cg_update(c, prec, c->s, h, has_loop);  // x,r update; z = P r; ||r||, <r,z>
@@ -640,7 +641,7 @@ int hdgb_pcg(hdgb_ctx* c, int variant, int prec, const double* F, double* x, dou
         if (h->done) break;
       }
     }
-    if (variant == HDGB_PLAIN && prec == HDGB_PREC_BLOCK) HDGB_CUDA(launch_x_final(c, c->s));  // last deferred x update
+    HDGB_CUDA(launch_x_final(c, c->s));  // the last deferred x update
     HDGB_CUDA(cudaMemcpyAsync(h, c->d_st, sizeof(CGState), cudaMemcpyDeviceToHost, c->s));
     HDGB_CUDA(cudaStreamSynchronize(c->s));
     if (use_graph) c->launches += c->graph_launches[variant][prec] * (int64_t)(h->it > 0 ? h->it : 1);

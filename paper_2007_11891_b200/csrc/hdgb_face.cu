@@ -33,7 +33,8 @@ enum { PW_PREC = 0, PW_INIT = 1, PW_UPDATE = 2 };
 constexpr int PW_U = 4;       // elements per thread per sweep
 constexpr int PW_GRID = 1184; // fixed grid (8 CTAs x 148 SMs)
 
-template <int N, int PREC, int FK, bool WITHZ>
+// NOX (PCG with the x update deferred into the next direction update): r -= alpha w only
+template <int N, int PREC, int FK, bool WITHZ, bool NOX = false>
 __global__ void __launch_bounds__(256) pw_kernel(FaceArgs a, const uint8_t* __restrict__ finfo, unsigned n) {
   constexpr unsigned N2 = N * N;
   pdl_trigger();
@@ -59,8 +60,10 @@ __global__ void __launch_bounds__(256) pw_kernel(FaceArgs a, const uint8_t* __re
           v0[k] = a.in[i];
           v1[k] = a.w[i];
         } else {
-          v0[k] = a.x[i];
-          v1[k] = a.p[i];
+          if (!NOX) {
+            v0[k] = a.x[i];
+            v1[k] = a.p[i];
+          }
           v2[k] = a.r[i];
           v3[k] = a.w[i];
         }
@@ -78,10 +81,13 @@ __global__ void __launch_bounds__(256) pw_kernel(FaceArgs a, const uint8_t* __re
         val = kind == HDGB_DIRICHLET ? 0.0 : v0[k] - v1[k];  // r = F - K x0 (solver.py:291)
         a.r[i] = val;
       } else {
-        double xv = v0[k], rv = v2[k];
-        xv += alpha * v1[k];  // x += alpha p  (solver.py:313)
+        double rv = v2[k];
+        if (!NOX) {
+          double xv = v0[k];
+          xv += alpha * v1[k];  // x += alpha p  (solver.py:313)
+          a.x[i] = xv;
+        }
         rv -= alpha * v3[k];  // r -= alpha w  (solver.py:314)
-        a.x[i] = xv;
         a.r[i] = rv;
         val = rv;
       }
@@ -480,7 +486,7 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
 }
 
 // ================================================================ deferred x update
-// block PCG: the last x += alpha p after the loop (every exit but a breakdown or a non-finite
+// the last x += alpha p after the PCG loop (every exit but a breakdown or a non-finite
 // residual follows an r update whose x update is still pending)
 __global__ void x_final_kernel(double* __restrict__ x, const double* __restrict__ p, int64_t n, const CGState* st) {
   if (st->status != HDGB_OK || st->it == 0) return;
@@ -492,11 +498,16 @@ __global__ void x_final_kernel(double* __restrict__ x, const double* __restrict_
 // ================================================================ CG direction update
 // p = z + beta p (solver.py:320) as its own pass, for the transformed PCG at the degrees where
 // folding it into the colour passes measured slower (hdgb_abi.cu, enqueue_iteration)
-__global__ void p_update_kernel(const double* __restrict__ z, double* __restrict__ p, int64_t n, const CGState* st) {
+// (with the deferred x += alpha_prev p_prev of the previous iteration)
+__global__ void p_update_kernel(const double* __restrict__ z, double* __restrict__ p, double* __restrict__ x, int64_t n,
+                                const CGState* st) {
   if (st->done) return;
-  const double beta = st->beta;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = fma(beta, p[i], z[i]);
+  const double beta = st->beta, alpha = st->alpha;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double po = p[i];
+    p[i] = fma(beta, po, z[i]);
+    x[i] = fma(alpha, po, x[i]);
+  }
 }
 
 // ================================================================ generic vectors
@@ -786,23 +797,23 @@ static FaceArgs base_args(hdgb_ctx* c, int prec) {
   return a;
 }
 
-template <int N, int PREC, int FK, bool WITHZ>
+template <int N, int PREC, int FK, bool WITHZ, bool NOX = false>
 static cudaError_t pw_launch(hdgb_ctx* c, const FaceArgs& a, cudaStream_t s) {
   const int64_t n = c->n_all;
   int grid = (int)min((int64_t)PW_GRID, (n + 256 * PW_U - 1) / (256 * PW_U));
   if (grid < 1) grid = 1;
-  cudaError_t le = launch_pdl(pw_kernel<N, PREC, FK, WITHZ>, dim3(grid), dim3(256), 0, s, a, c->d_finfo, (unsigned)n);
+  cudaError_t le = launch_pdl(pw_kernel<N, PREC, FK, WITHZ, NOX>, dim3(grid), dim3(256), 0, s, a, c->d_finfo, (unsigned)n);
   c->launches++;
   return le;
 }
 
-template <int N, int FK, bool WITHZ>
+template <int N, int FK, bool WITHZ, bool NOX = false>
 static cudaError_t pw_prec(hdgb_ctx* c, int prec, const FaceArgs& a, cudaStream_t s) {
   switch (prec) {
-    case HDGB_PREC_NONE: return pw_launch<N, HDGB_PREC_NONE, FK, WITHZ>(c, a, s);
-    case HDGB_PREC_DIAG_NODAL: return pw_launch<N, HDGB_PREC_DIAG_NODAL, FK, WITHZ>(c, a, s);
-    case HDGB_PREC_DIAG_EIGEN: return pw_launch<N, HDGB_PREC_DIAG_EIGEN, FK, WITHZ>(c, a, s);
-    case HDGB_PREC_BLOCK: return pw_launch<N, HDGB_PREC_NONE, FK, false>(c, a, s);  // r only; block follows
+    case HDGB_PREC_NONE: return pw_launch<N, HDGB_PREC_NONE, FK, WITHZ, NOX>(c, a, s);
+    case HDGB_PREC_DIAG_NODAL: return pw_launch<N, HDGB_PREC_DIAG_NODAL, FK, WITHZ, NOX>(c, a, s);
+    case HDGB_PREC_DIAG_EIGEN: return pw_launch<N, HDGB_PREC_DIAG_EIGEN, FK, WITHZ, NOX>(c, a, s);
+    case HDGB_PREC_BLOCK: return pw_launch<N, HDGB_PREC_NONE, FK, false, NOX>(c, a, s);  // r only; block follows
   }
   return cudaErrorInvalidValue;
 }
@@ -890,6 +901,7 @@ static cudaError_t face_n(hdgb_ctx* c, int op, int prec, const FaceArgs& a, cuda
         to.set(N);
         return fx_launch<N, FX_UPDATE, 1>(c, b, c->h_tab.data() + to.St, c->h_tab.data() + to.S, N * N, s);
       }
+      if (c->pupd_x) return pw_prec<N, PW_UPDATE, true, true>(c, prec, a, s);  // x update deferred
       if ((e = pw_prec<N, PW_UPDATE, true>(c, prec, a, s)) != cudaSuccess) return e;
       if (prec == HDGB_PREC_BLOCK) {
         FaceArgs b = a;
@@ -1007,7 +1019,8 @@ cudaError_t launch_x_final(hdgb_ctx* c, cudaStream_t s) {
 cudaError_t launch_p_update(hdgb_ctx* c, cudaStream_t s) {
   double* v = c->d_vec;
   const int64_t n = c->n_all;
-  p_update_kernel<<<grid_for(n, 1024), 1024, 0, s>>>(v + V_Z * c->vstride, v + V_P * c->vstride, n, c->d_st);
+  p_update_kernel<<<grid_for(n, 1024), 1024, 0, s>>>(v + V_Z * c->vstride, v + V_P * c->vstride,
+                                                      v + V_X * c->vstride, n, c->d_st);
   c->launches++;
   return cudaGetLastError();
 }

@@ -124,6 +124,7 @@ struct OpArgs {
   double* part;          // CG mode: per-CTA partials of <p, w>
   const double* z;       // CG mode, fused direction update: z (u = p is updated in place via pout)
   double* pout;
+  double* xout;          // CG mode, fused direction update: x (deferred x += alpha_prev p_prev)
 };
 
 struct FaceArgs {

@@ -133,11 +133,11 @@ struct OpVCfg {
 #else
   static constexpr bool DZS = N >= 12;
 #endif
-  // PUPD (transformed PCG, direction update fused into colour pass 0): z staged next to p
-  // z staging (PUPD) starts 16-byte aligned after the volume and the dz_inv copy
+  // PUPD (transformed PCG, direction and deferred x updates fused into colour pass 0): z and x
+  // staged next to p, starting 16-byte aligned after the volume and the dz_inv copy
   static constexpr int ZOFF = (G * (2 * FS + VS) + (DZS ? N * NQ : 0) + 1) / 2 * 2;
   __host__ __device__ static constexpr int smem_doubles(bool pupd = false) {
-    return pupd ? ZOFF + 2 * G * FS : G * (2 * FS + VS) + (DZS ? N * NQ : 0);
+    return pupd ? ZOFF + 4 * G * FS : G * (2 * FS + VS) + (DZS ? N * NQ : 0);
   }
 };
 
@@ -170,13 +170,17 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
   // pass: colour 0 updates every face of its elements while staging them and, in a tail loop,
   // the boundary faces whose only element is colour 1; the new p is written back, so colour 1
   // and the x update read it
+  // (x += alpha_prev p_prev, solver.py:313, deferred from the previous iteration, rides along)
   constexpr bool PUPD = CG && (MODE & 8) && COLOR == 0;
   pdl_trigger();
-  double beta = 0.0;
+  double beta = 0.0, alpha_prev = 0.0;
   if (CG) {
     pdl_wait();
     if (a.st->done) return;
-    if (PUPD) beta = a.st->beta;
+    if (PUPD) {
+      beta = a.st->beta;
+      alpha_prev = a.st->alpha;
+    }
   }
   constexpr bool TMA = C::TMA;
   constexpr int FSTR = C::FSTR;
@@ -229,7 +233,8 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
       }
     }
   };
-  double* sZ0 = smem + C::ZOFF;  // PUPD: 2 x G x [6][FSTR] staged z
+  double* sZ0 = smem + C::ZOFF;      // PUPD: 2 x G x [6][FSTR] staged z
+  double* sX0 = sZ0 + 2 * G * FS;    // PUPD: 2 x G x [6][FSTR] staged x
   if (TMA && tid == 0) {
     mbar_init(&sBar[0], 1);
     mbar_init(&sBar[1], 1);
@@ -241,7 +246,7 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
   auto stage_tma = [&](const ElemInfo* inf, double* buf, int bi) {
     if (tid >= 32) return;
     constexpr uint32_t CNT = (NQ & 1) ? NQ + 1 : NQ;  // doubles per face copy (even)
-    constexpr int NC = PUPD ? 12 : 6;
+    constexpr int NC = PUPD ? 18 : 6;
     if (tid == 0) {
       uint32_t nval = 0;
       for (int ee = 0; ee < G; ++ee) nval += inf[ee].valid ? 1u : 0u;
@@ -254,8 +259,8 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
       if (!inf[ee].valid) continue;
       const unsigned off = inf[ee].off[sface];
       const unsigned lo = (NQ & 1) ? (off & ~1u) : off;
-      double* dst = (k < 6 ? buf : sZ0 + bi * G * FS) + ee * FS + sface * FSTR;
-      bulk_g2s(dst, (k < 6 ? a.u : a.z) + lo, CNT * 8u, &sBar[bi]);
+      double* dst = (k < 6 ? buf : (k < 12 ? sZ0 : sX0) + bi * G * FS) + ee * FS + sface * FSTR;
+      bulk_g2s(dst, (k < 6 ? a.u : (k < 12 ? a.z : a.xout)) + lo, CNT * 8u, &sBar[bi]);
     }
   };
   auto stage = [&](const ElemInfo* inf, double* buf, int bi) {
@@ -269,8 +274,11 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
       for (int s = 0; s < 6; ++s) cp_async8(dst + s * NQ, a.u + (inf[e].off[s] + (unsigned)q));
       if (PUPD) {
         double* dz = sZ0 + bi * G * FS + e * FS + q;
+        double* dx = sX0 + bi * G * FS + e * FS + q;
 #pragma unroll
         for (int s = 0; s < 6; ++s) cp_async8(dz + s * NQ, a.z + (inf[e].off[s] + (unsigned)q));
+#pragma unroll
+        for (int s = 0; s < 6; ++s) cp_async8(dx + s * NQ, a.xout + (inf[e].off[s] + (unsigned)q));
       }
     }
   };
@@ -310,12 +318,15 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
     if (PUPD && on) {  // position q of every face is this thread's own copy (cp.async) or
                        // complete for every thread (TMA barrier): no extra CTA barrier needed
       const double* sZ = sZ0 + buf * G * FS + (act ? e : 0) * FS;
+      const double* sX = sX0 + buf * G * FS + (act ? e : 0) * FS;
 #pragma unroll
       for (int s = 0; s < 6; ++s) {
         double* fp = fb[s] + q;
-        const double pn = fma(beta, *fp, sZ[(fb[s] - sFw) + q]);
+        const int64_t so = (fb[s] - sFw) + q;
+        const double po = *fp, pn = fma(beta, po, sZ[so]);
         *fp = pn;
         a.pout[off[s]] = pn;
+        a.xout[off[s]] = fma(alpha_prev, po, sX[so]);
       }
     }
     __syncthreads();  // staged faces (and their update) visible to the whole CTA
@@ -420,7 +431,9 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
       const int64_t fid = g.foff[d] + face_lo(g, d, c[0], c[1], c[2]) + side * face_step(g, d);
       for (int qq = lane; qq < NQ; qq += 32) {
         const int64_t o = fid * NQ + qq;
-        a.pout[o] = fma(beta, a.u[o], a.z[o]);
+        const double po = a.u[o];
+        a.pout[o] = fma(beta, po, a.z[o]);
+        a.xout[o] = fma(alpha_prev, po, a.xout[o]);
       }
     }
   }
@@ -508,9 +521,10 @@ static cudaError_t launch_t(hdgb_ctx* c, const double* u, double* r, cudaStream_
   const int64_t nslab = (g.n3 + layers - 1) / layers;
   cudaError_t e;
   if constexpr (!PLAIN && (MODE & 1)) {
-    if (c->pupd_z) {  // transformed PCG: direction update fused into the colour passes (one slab)
+    if (c->pupd_z && c->pupd_x) {  // transformed PCG: direction update fused into the colour passes (one slab)
       a.z = c->pupd_z;
       a.pout = const_cast<double*>(u);
+      a.xout = c->pupd_x;
       const int64_t t1 = g.n3 * per_k;
       e = c->uniform ? launch_any<N, false, MODE | 8, 0>(c, a, 0, t1, s)
                      : launch_any<N, false, MODE | 10, 0>(c, a, 0, t1, s);
