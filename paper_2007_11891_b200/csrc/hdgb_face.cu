@@ -170,10 +170,20 @@ struct FxCfg {
   static constexpr int pad16(int x, int r) { return x + (((r - x) % 16) + 16) % 16; }
   static constexpr int WP = pad16(N * NP, N % 16);   // exchange face pitch, = N (mod 16)
   static constexpr int BATW = (FPW * N2 + 2 + 1) / 2 * 2;  // staged batch (+ alignment slack), even
+// the PCG pre-transform (z, p and x staged) keeps 2 stages: 3 measured slower at p = 8
+// (block PCG 809 vs 790 us/iter; more CTAs per SM, MINB 3, no further gain)
+#ifndef HDGB_FXT_S
+#define HDGB_FXT_S 2
+#endif
+#ifndef HDGB_FXU_S
+#define HDGB_FXU_S 0
+#endif
 #ifdef HDGB_FX_S
   static constexpr int S = HDGB_FX_S;
 #else
-  static constexpr int S = N <= 11 ? 3 : 2;          // ring stages per group
+  static constexpr int S = (FK == FX_TRANSFORM && CG && HDGB_FXT_S) ? HDGB_FXT_S
+                           : (FK == FX_UPDATE && CG && HDGB_FXU_S) ? HDGB_FXU_S
+                                                                   : (N <= 11 ? 3 : 2);  // ring stages per group
 #endif
   static constexpr int EPT = (FPW * N2 + GT - 1) / GT;  // epilogue values per thread
   // FX_POST stages u next to G with the same bulk copies for N <= 11 (measured: p = 8 plain
