@@ -181,8 +181,12 @@ struct FxCfg {
 #ifdef HDGB_FX_S
   static constexpr int S = HDGB_FX_S;
 #else
+#ifndef HDGB_FXPC_S
+#define HDGB_FXPC_S 0
+#endif
   static constexpr int S = (FK == FX_TRANSFORM && CG && HDGB_FXT_S) ? HDGB_FXT_S
                            : (FK == FX_UPDATE && CG && HDGB_FXU_S) ? HDGB_FXU_S
+                           : (FK == FX_POST && CG && HDGB_FXPC_S) ? HDGB_FXPC_S
                                                                    : (N <= 11 ? 3 : 2);  // ring stages per group
 #endif
   static constexpr int EPT = (FPW * N2 + GT - 1) / GT;  // epilogue values per thread
@@ -218,8 +222,13 @@ struct FxCfg {
 #ifndef HDGB_FXT_MINB
 #define HDGB_FXT_MINB 2
 #endif
+#ifndef HDGB_FXPC_MINB
+#define HDGB_FXPC_MINB 2
+#endif
   static constexpr int MINB = ((FK == FX_POST && OPS == 2) || (FK == FX_PREC && N >= 8)) ? 3
-                              : (FK == FX_UPDATE ? HDGB_FXU_MINB : (FK == FX_TRANSFORM && CG ? HDGB_FXT_MINB : 2));
+                              : (FK == FX_UPDATE ? HDGB_FXU_MINB
+                                                 : (FK == FX_TRANSFORM && CG ? HDGB_FXT_MINB
+                                                                             : (FK == FX_POST && CG ? HDGB_FXPC_MINB : 2)));
 #endif
 };
 
