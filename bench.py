@@ -561,8 +561,8 @@ def run_ours(args):
                      "converged": rep.converged, "relres": rep.relative_residual,
                      "pcg_ms": rep.wall_time * 1e3,
                      "note": "hb.solve(u0=0, f, ...) wall clock: f upload, device RHS, fused block-PCG, device "
-                             "interior recovery, (u, q) download to numpy (4 x n_e (p+1)^3 doubles = 96 MB at "
-                             "config 2, which dominates the wall time)"}
+                             "interior recovery, (u, q) download to new numpy arrays (4 x n_e (p+1)^3 doubles = 96 MB at "
+                             "config 2: page-locked staging + threaded host copy)"}
 
     # ---- FP64 view of the plain operator (FP64-bound for p >~ 3; reference FlopCounter counts)
     import ctypes

@@ -295,6 +295,29 @@ class DeviceContext:
                                              self.stream()))
         return x
 
+    def download(self, tensors):
+        """Device tensors -> new numpy arrays: one D2H copy into a cached page-locked staging buffer,
+        then a multi-threaded host copy (the page faults of the fresh arrays dominate otherwise)."""
+        import torch
+
+        sizes = [t.numel() for t in tensors]
+        total = sum(sizes)
+        stage = getattr(self, "_stage", None)
+        if stage is None or stage.numel() < total:
+            stage = self._stage = torch.empty(total, dtype=torch.float64).pin_memory()
+        o = 0
+        for t, k in zip(tensors, sizes):
+            stage[o:o + k].copy_(t.reshape(-1), non_blocking=True)
+            o += k
+        torch.cuda.current_stream(self.device).synchronize()
+        outs, o = [], 0
+        for t, k in zip(tensors, sizes):
+            a = np.empty(tuple(t.shape))
+            torch.from_numpy(a).view(-1).copy_(stage[o:o + k])
+            outs.append(a)
+            o += k
+        return outs
+
     def recover_interior(self, f, trace):
         """(u, (q1, q2, q3)) from f and the all-face trace (solver.py:254-279), device tensors."""
         import torch

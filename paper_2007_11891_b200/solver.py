@@ -530,7 +530,8 @@ def _solve_device(u0, f, g_D, g_N, cfg, ctx, transformed):
     mesh, p = ctx.mesh, ctx.basis.p
     dev = f"cuda:{dc.device}"
     counter = getattr(ctx, "counter", None)
-    F = dc.build_rhs(f)
+    fd = torch.as_tensor(np.ascontiguousarray(f), dtype=torch.float64).to(dev)  # uploaded once: RHS and recovery
+    F = dc.build_rhs(fd)
     if g_N is not None:  # Neumann data (solver.py:233-237)
         neu = FluxField(mesh, p)
         for d in range(3):
@@ -574,8 +575,9 @@ def _solve_device(u0, f, g_D, g_N, cfg, ctx, transformed):
         x = dc.transform(x, np.ascontiguousarray(ctx.basis.S))
     if lift is not None:
         x += lift  # _restore_dirichlet: Dirichlet slots are zero after the solve
-    u, qs = dc.recover_interior(f, x)
-    return (u.cpu().numpy(), tuple(q.cpu().numpy() for q in qs),
+    u, qs = dc.recover_interior(fd, x)
+    u, *qs = dc.download([u, *qs])
+    return (u, tuple(qs),
             SolveReport(iters, relres, conv, wall, wall / max(iters, 1), None if counter is None else flops))
 
 
