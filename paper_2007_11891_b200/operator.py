@@ -423,7 +423,7 @@ def transform_faces(field, A, counter=None, ctx=None):
     if isinstance(field, DeviceFluxField):
         return DeviceFluxField(field.mesh, field.p, dc.transform(field.flat, A))
     u = torch.from_numpy(np.concatenate([np.asarray(a, dtype=np.float64).ravel() for a in field.data]))
-    out = dc.transform(u.to(f"cuda:{dc.device}"), A).cpu().numpy()
+    out = dc.download([dc.transform(u.to(f"cuda:{dc.device}"), A)])[0]
     res, off = [], 0
     for d in range(3):
         cnt = field.mesh.n_faces[d] * n * n

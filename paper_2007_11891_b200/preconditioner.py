@@ -52,7 +52,7 @@ class _DevicePrecBase:
         if isinstance(residual, DeviceFluxField):
             return DeviceFluxField(residual.mesh, residual.p, self._run(dc, residual.flat))
         u = torch.from_numpy(np.concatenate([np.asarray(a, dtype=np.float64).ravel() for a in residual.data]))
-        z = self._run(dc, u.to(f"cuda:{dc.device}")).cpu().numpy()
+        z = dc.download([self._run(dc, u.to(f"cuda:{dc.device}"))])[0]
         return type(residual)(residual.mesh, residual.p, _split_host(z, residual.mesh, n))
 
     def apply_packed(self, vec, counter=None):
@@ -65,7 +65,7 @@ class _DevicePrecBase:
         if isinstance(vec, torch.Tensor):
             return dc.pack(self._run(dc, dc.unpack(vec.contiguous())))
         v = torch.from_numpy(np.ascontiguousarray(vec, dtype=np.float64)).to(f"cuda:{dc.device}")
-        return dc.pack(self._run(dc, dc.unpack(v))).cpu().numpy()
+        return dc.download([dc.pack(self._run(dc, dc.unpack(v)))])[0]
 
     def _table(self, kind):
         dc = self._dc

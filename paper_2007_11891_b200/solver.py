@@ -124,7 +124,7 @@ class DeviceOperator:
         if isinstance(v, torch.Tensor):
             return dc.pack(dc.apply(dc.unpack(v.contiguous()), self.variant))
         vd = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(f"cuda:{dc.device}")
-        return dc.pack(dc.apply(dc.unpack(vd), self.variant)).cpu().numpy()
+        return dc.download([dc.pack(dc.apply(dc.unpack(vd), self.variant))])[0]
 
 
 def _fused_plan(apply_K, apply_P):
@@ -156,7 +156,7 @@ def _pcg_fused(plan, F, x0, rtol, atol, max_iters):
     it, rel, conv = dc.pcg(variant, kind, Fa, xa, rtol, atol, max_iters)
     x = dc.pack(xa)
     if as_np:
-        x = x.cpu().numpy()
+        x = dc.download([x])[0]
     return x, it, rel, conv
 
 
