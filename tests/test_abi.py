@@ -3,6 +3,7 @@ import ctypes
 import os
 import re
 import subprocess
+import sys
 
 import pytest
 
@@ -60,3 +61,20 @@ def test_ctx_create_rejects_bad_arguments_without_gpu(lib_path):
     assert rc == _lib.EINVAL
     with pytest.raises(ValueError):
         _lib.check(rc)
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: without the built library the hot path raises instead of computing."""
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "from paper_2007_11891_b200 import _lib\n"
+        "try:\n"
+        "    _lib.lib()\n"
+        "except _lib.LibraryMissing as e:\n"
+        "    print('raised', e)\n"
+        "else:\n"
+        "    print('loaded')\n" % ROOT)
+    env = dict(os.environ, HDGB_LIB=str(tmp_path / "absent.so"))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.startswith("raised"), out.stdout
