@@ -163,7 +163,15 @@ struct FxCfg {
 #ifndef HDGB_FX_WARPS
 #define HDGB_FX_WARPS 4
 #endif
-  static constexpr int WARPS = HDGB_FX_WARPS;        // warps per CTA
+// the plain operator's face transforms (pre-transform, epilogue) at N >= 13 run two groups per
+// CTA: p = 16 plain apply 719 -> 676 us, block PCG 1643 -> 1508 us/iter (p = 14: 1260 -> 1182);
+// slower from N = 11 down (p = 10 plain 444 -> 635 us)
+#ifndef HDGB_FX_WIDE_N
+#define HDGB_FX_WIDE_N 13
+#endif
+  // warps per CTA
+  static constexpr int WARPS =
+      (N >= HDGB_FX_WIDE_N && (FK == FX_TRANSFORM || FK == FX_POST)) ? 2 * HDGB_FX_WARPS : HDGB_FX_WARPS;
   static constexpr int NG = WARPS / GW;              // independent groups per CTA
   static constexpr int NT = 32 * WARPS;
   static constexpr int NP = 17;                      // exchange row pitch, = 1 (mod 16)
