@@ -265,6 +265,51 @@ def _large_point(hb, p, m, lam, flush, stream, hbm, fp64_peak, reps=10, mesh=Non
     return out
 
 
+def _config5_solve(hb, stream):
+    """BASELINE config 5 full solve on one GPU: 128^3, p = 8, lambda = 1, f from
+    u = sin(pi x) sin(pi y) sin(pi z), preconditioned CG to 1e-10 from a zero trace (block and
+    transformed pipelines), everything device-resident (f is 12 GB: built on the device from the
+    per-axis node coordinates), then the interior recovery and the max error against u."""
+    import torch
+
+    m, p, lam = 128, 8, 1.0
+    mesh = hb.Mesh((m, m, m))
+    ctx = hb.make_context(mesh, p, hb.SolverConfig(lam=lam))
+    dc = hb.device_context(ctx)
+    X = mesh.element_node_grids(ctx.basis.nodes)
+    s = [torch.from_numpy(np.sin(math.pi * np.ascontiguousarray(X[d]).reshape(mesh.n_elements, p + 1))).cuda()
+         for d in range(3)]
+    fdev = (lam + 3 * math.pi ** 2) * s[0][:, :, None, None] * s[1][:, None, :, None] * s[2][:, None, None, :]
+    del s, X
+    F = dc.build_rhs(fdev)
+    dc.zero_dirichlet(F)
+    out = {"mesh": "128^3, p=8, lambda=1", "trace_unknowns": mesh.n_trace_unknowns(p)}
+    S = np.ascontiguousarray(ctx.basis.S)
+    for name, variant, kind in (("block", 0, 1), ("transformed", 1, 3)):
+        rhs = dc.zero_dirichlet(dc.transform(F, np.ascontiguousarray(S.T))) if variant == 1 else F
+        x = torch.zeros_like(F)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        it, rel, conv = dc.pcg(variant, kind, rhs, x, 1e-10, 0.0, 10000)
+        b.record(stream)
+        b.synchronize()
+        t = a.elapsed_time(b) * 1e-3
+        if variant == 1:
+            x = dc.transform(x, S)
+        u, _ = dc.recover_interior(fdev, x)
+        err = float(torch.max(torch.abs(u - fdev / (lam + 3 * math.pi ** 2))))
+        out[name] = {"iterations": it, "converged": conv, "relres": rel, "pcg_ms": t * 1e3,
+                     "ms_per_iter": t / max(it, 1) * 1e3,
+                     "ps_per_unknown_per_iter": t / max(it, 1) / out["trace_unknowns"] * 1e12, "err_max": err}
+        del u, x, rhs
+        torch.cuda.empty_cache()
+    del dc, ctx, fdev, F
+    torch.cuda.empty_cache()
+    return out
+
+
 def _config4(hb, flush, stream, hbm, fp64_peak):
     """non-uniform 64x32x32 grid on [0,2]x[0,1]^2, p = 7, lambda = 100, per-axis
     widths uniform[0.5, 2] x mean from rng(7) (x, y, z order) rescaled to the box, tau_hat = 0.390625
@@ -590,6 +635,7 @@ def run_ours(args):
             large["config4_64x32x32_p7_nonuniform"] = _config4(hb, flush, stream, hbm, fp64_peak.value)
         if args.config5:
             large["config5_128^3_p8"] = _large_point(hb, 8, 128, 1.0, flush, stream, hbm, fp64_peak.value, reps=5)
+            large["config5_128^3_p8"]["solve"] = _config5_solve(hb, stream)
 
     # ---- CPU oracle on this host (rank 0, N=1 only)
     cpu = None
