@@ -206,10 +206,15 @@ struct FxCfg {
                              : ((FK == FX_POST && HDGB_FX_POST_TMA) || (FK == FX_TRANSFORM && CG) || (FK == FX_UPDATE && CG)) ? 2
                                                                                                                : 1;
 #else
+#ifndef HDGB_FXPC_TMA
+#define HDGB_FXPC_TMA 0
+#endif
   // staged operands: FX_TRANSFORM CG = 1: z, p; CG = 2: z, p, x; FX_UPDATE CG = 1: r, w
   static constexpr int OPS = (FK == FX_TRANSFORM && CG == 2) ? 3
-                             : ((FK == FX_POST && !CG && N <= 11) || (FK == FX_TRANSFORM && CG) || (FK == FX_UPDATE && CG)) ? 2
-                                                                                                                  : 1;
+                             : ((FK == FX_POST && (!CG || HDGB_FXPC_TMA) && N <= 11) || (FK == FX_TRANSFORM && CG) ||
+                                (FK == FX_UPDATE && CG))
+                                   ? 2
+                                   : 1;
 #endif
   static constexpr bool BLOCK = FK == FX_PREC || FK == FX_INIT || FK == FX_UPDATE;
   // per-group slice, 128-byte aligned (bulk-copy destinations need 16)
@@ -233,7 +238,7 @@ struct FxCfg {
 #ifndef HDGB_FXPC_MINB
 #define HDGB_FXPC_MINB 2
 #endif
-  static constexpr int MINB = ((FK == FX_POST && OPS == 2) || (FK == FX_PREC && N >= 8)) ? 3
+  static constexpr int MINB = ((FK == FX_POST && !CG && OPS == 2) || (FK == FX_PREC && N >= 8)) ? 3
                               : (FK == FX_UPDATE ? HDGB_FXU_MINB
                                                  : (FK == FX_TRANSFORM && CG ? HDGB_FXT_MINB
                                                                              : (FK == FX_POST && CG ? HDGB_FXPC_MINB : 2)));
