@@ -246,6 +246,32 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
   CK(cudaMemset(c->d_st, 0, sizeof(CGState)));
   CK(cudaMallocHost(&c->h_st, sizeof(CGState)));
   memset(c->h_st, 0, sizeof(CGState));
+  {  // eigenvector parities for the folded face products (see mv_n2e in hdgb_face.cu)
+    hdgb::TabOff to;
+    to.set(c->N);
+    const double* S = c->h_tab.data() + to.S;
+    const int N = c->N;
+    double mx = 0.0;
+    for (int q = 0; q < N * N; ++q) mx = fabs(S[q]) > mx ? fabs(S[q]) : mx;
+    uint32_t sig = 0;
+    bool ok = N <= 32;
+    for (int a = 0; a < N && ok; ++a) {
+      double corr = 0.0;
+      for (int i = 0; i < N; ++i) corr += S[i * N + a] * S[(N - 1 - i) * N + a];
+      const double sg = corr >= 0.0 ? 1.0 : -1.0;
+      if (sg > 0) sig |= 1u << a;
+      for (int i = 0; i < N; ++i)
+        if (fabs(S[(N - 1 - i) * N + a] - sg * S[i * N + a]) > 1e-9 * mx) ok = false;
+    }
+    // folded products from N = 13 up (p = 12: plain apply 549 -> 459 us, block PCG 1085 ->
+    // 800 us/iter; p = 16: block preconditioner 374 -> 169 us); below, the unfolded products
+    // measured faster (p = 6 block PCG 793 vs 839 us/iter, p = 9 813 vs 844)
+    const char* fe = getenv("HDGB_FOLD");
+    const char* fn = getenv("HDGB_FOLD_NMIN");
+    const int nmin = fn ? atoi(fn) : 13;
+    c->sig = sig;
+    c->fold_ok = ok && !(fe && atoi(fe) == 0) && N >= nmin;
+  }
   CK(launch_build_tables(c, c->s));
   CK(cudaStreamSynchronize(c->s));
   // validate the preconditioner diagonals on unknown faces (preconditioner.py:89-90, 146-147)

@@ -256,12 +256,76 @@ __device__ __forceinline__ void line_mv(const double* __restrict__ M, const doub
     for (int j = 0; j < N; ++j) y[j] = fma(M[j * N + i], x[i], y[j]);
 }
 
+// Parity folding (even-odd decomposition).  The GLL nodes are symmetric about the element
+// centre, so every eigenvector of the 1D problem is even or odd: S[N-1-i][a] = sig_a S[i][a]
+// (sig_a = +-1, a pattern that depends on p and tau and is read from S at context creation).
+// T = S^T M, M S and S inherit it, so each 1D product needs about half of its N^2 FMAs:
+//  nodal -> eigen (T, S^T):  y_a = sum_{i<N/2} Af[a][i] (x_i + sig_a x_{N-1-i})  (+ mid term)
+//  eigen -> nodal (M S, S):  x_i, x_{N-1-i} = E_i +- O_i, E (O) summing the even (odd) y_a
+// Af holds the folded (symmetrised) halves; sig is a uniform kernel parameter, so the choice of
+// chain per eigen index is a warp-uniform branch.
+template <int N>
+__device__ __forceinline__ void mv_n2e(const double* __restrict__ Af, uint32_t sig, const double* x, double* y) {
+  constexpr int H = N / 2, HC = (N + 1) / 2;
+  double e[HC], o[H > 0 ? H : 1];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    e[i] = x[i] + x[N - 1 - i];
+    o[i] = x[i] - x[N - 1 - i];
+  }
+  if (N & 1) e[H] = x[H];
+#pragma unroll
+  for (int a = 0; a < N; ++a) {
+    if (sig >> a & 1u) {
+      double acc = Af[a * HC] * e[0];
+#pragma unroll
+      for (int i = 1; i < HC; ++i) acc = fma(Af[a * HC + i], e[i], acc);
+      y[a] = acc;
+    } else {
+      double acc = Af[a * HC] * o[0];
+#pragma unroll
+      for (int i = 1; i < H; ++i) acc = fma(Af[a * HC + i], o[i], acc);
+      y[a] = acc;
+    }
+  }
+}
+template <int N>
+__device__ __forceinline__ void mv_e2n(const double* __restrict__ Af, uint32_t sig, const double* y, double* x) {
+  constexpr int H = N / 2, HC = (N + 1) / 2;
+  double E[HC], O[H > 0 ? H : 1];
+#pragma unroll
+  for (int i = 0; i < HC; ++i) E[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < H; ++i) O[i] = 0.0;
+#pragma unroll
+  for (int a = 0; a < N; ++a) {
+    if (sig >> a & 1u) {
+#pragma unroll
+      for (int i = 0; i < HC; ++i) E[i] = fma(Af[i * N + a], y[a], E[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < H; ++i) O[i] = fma(Af[i * N + a], y[a], O[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    x[i] = E[i] + O[i];
+    x[N - 1 - i] = E[i] - O[i];
+  }
+  if (N & 1) x[H] = E[H];
+}
+
 // A: forward 1D matrix (S^T, T, MS or the user's A), B: backward (S); FX_POST keeps the
-// quadrature weights in B[0..N-1].
+// quadrature weights in B[0..N-1].  fold: use the parity-folded Af / Bf (A is nodal -> eigen
+// except for FX_POST, B is eigen -> nodal).
 template <int N>
 struct FxMats {
   double A[N * N];
   double B[N * N];
+  double Af[N * N];
+  double Bf[N * N];
+  uint32_t sig;
+  int fold;
 };
 
 
@@ -315,6 +379,18 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
   }
   __syncthreads();  // the only CTA-wide barrier: tables and barrier init
   if (!EARLY) pdl_wait();  // inputs come from earlier kernels
+  auto mvA = [&](const double* xin, double* yout) {
+    if (M.fold) {
+      if (FK == FX_POST) mv_e2n<N>(M.Af, M.sig, xin, yout);
+      else mv_n2e<N>(M.Af, M.sig, xin, yout);
+    } else {
+      line_mv<N>(M.A, xin, yout);
+    }
+  };
+  auto mvB = [&](const double* xin, double* yout) {
+    if (M.fold) mv_e2n<N>(M.Bf, M.sig, xin, yout);
+    else line_mv<N>(M.B, xin, yout);
+  };
   auto gsync = [&]() {
     if (GW == 1) {
       __syncwarp();
@@ -399,7 +475,7 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
 #pragma unroll
         for (int i = 0; i < N; ++i) x[i] = xs[i * N];
       }
-      line_mv<N>(M.A, x, y);
+      mvA(x, y);
       double* ws = sW + f * WP + l;
 #pragma unroll
       for (int j = 0; j < N; ++j) ws[j * NP] = y[j];
@@ -409,7 +485,7 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
       double* wr = sW + f * WP + l * NP;
 #pragma unroll
       for (int c = 0; c < N; ++c) z[c] = wr[c];
-      line_mv<N>(M.A, z, y);
+      mvA(z, y);
       if (BLOCK) {  // * y^-1 (preconditioner.py:100-104), then pass 3 along the second index
         if (a.ycls) {
           const double* yi = sY + finfo_cls(inf) * N2 + l * N;
@@ -420,7 +496,7 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
 #pragma unroll
           for (int kk = 0; kk < N; ++kk) y[kk] *= __ldg(yi + kk);
         }
-        line_mv<N>(M.B, y, z);
+        mvB(y, z);
 #pragma unroll
         for (int kk = 0; kk < N; ++kk) wr[kk] = z[kk];
       } else if (ODD) {  // result row straight into the consumed stage, contiguous
@@ -438,7 +514,7 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
         double* wc = sW + f * WP + l;
 #pragma unroll
         for (int j = 0; j < N; ++j) z[j] = wc[j * NP];
-        line_mv<N>(M.B, z, y);
+        mvB(z, y);
         const int kind = finfo_kind(inf);
         if (kind == HDGB_DIRICHLET) {  // zero_dirichlet (preconditioner.py:107)
 #pragma unroll
@@ -853,14 +929,41 @@ static cudaError_t pw_prec(hdgb_ctx* c, int prec, const FaceArgs& a, cudaStream_
 // Launch a face-block kernel with its 1D matrices (host copies, passed by value) on a grid
 // of at most one resident wave; the grid is fixed per device, so the reductions of the
 // CG variants are reproducible.
+// parity-folded halves (see mv_n2e / mv_e2n), symmetrised: 0.5 (A[.][i] + sig A[.][N-1-i])
+static void fold_n2e(const double* A, int N, uint32_t sig, double* Af) {  // A[a][i], rows a eigen
+  const int H = N / 2, HC = (N + 1) / 2;
+  for (int a = 0; a < N; ++a) {
+    const double sg = (sig >> a & 1u) ? 1.0 : -1.0;
+    for (int i = 0; i < H; ++i) Af[a * HC + i] = 0.5 * (A[a * N + i] + sg * A[a * N + N - 1 - i]);
+    if (N & 1) Af[a * HC + H] = sg > 0 ? A[a * N + H] : 0.0;
+  }
+}
+static void fold_e2n(const double* A, int N, uint32_t sig, double* Af) {  // A[i][a], rows i nodal
+  const int H = N / 2;
+  for (int a = 0; a < N; ++a) {
+    const double sg = (sig >> a & 1u) ? 1.0 : -1.0;
+    for (int i = 0; i < H; ++i) Af[i * N + a] = 0.5 * (A[i * N + a] + sg * A[(N - 1 - i) * N + a]);
+    if (N & 1) Af[H * N + a] = sg > 0 ? A[H * N + a] : 0.0;
+  }
+}
+
 template <int N, int FK, int CG = 0>
 static cudaError_t fx_launch(hdgb_ctx* c, const FaceArgs& a, const double* Ah, const double* Bh, int nb_b,
-                             cudaStream_t s) {
+                             cudaStream_t s, int fold = 0) {
   using C = FxCfg<N, FK, CG>;
   FxMats<N> M;
   for (int q = 0; q < N * N; ++q) {
     M.A[q] = Ah[q];
     M.B[q] = q < nb_b ? Bh[q] : 0.0;
+    M.Af[q] = 0.0;
+    M.Bf[q] = 0.0;
+  }
+  M.fold = fold && c->fold_ok;
+  M.sig = c->sig;
+  if (M.fold) {
+    if (FK == FX_POST) fold_e2n(Ah, N, c->sig, M.Af);
+    else fold_n2e(Ah, N, c->sig, M.Af);
+    if (nb_b == N * N) fold_e2n(Bh, N, c->sig, M.Bf);
   }
   const size_t smem = sizeof(double) * C::smem_doubles();
   auto k = fx_kernel<N, FK, CG>;
@@ -881,8 +984,8 @@ template <int N, int FK>
 static cudaError_t blk_launch(hdgb_ctx* c, const FaceArgs& a, cudaStream_t s) {
   TabOff to;
   to.set(N);
-  if (FK == FX_TRANSFORM) return fx_launch<N, FK>(c, a, a.A, nullptr, 0, s);
-  return fx_launch<N, FK>(c, a, c->h_tab.data() + to.St, c->h_tab.data() + to.S, N * N, s);
+  if (FK == FX_TRANSFORM) return fx_launch<N, FK>(c, a, a.A, nullptr, 0, s, a.fold);
+  return fx_launch<N, FK>(c, a, c->h_tab.data() + to.St, c->h_tab.data() + to.S, N * N, s, 1);
 }
 
 // plain-operator epilogue: r = coef (w (x) w) u - (MS (x) MS) G, in place over G = r
@@ -897,7 +1000,7 @@ cudaError_t launch_plain_post(hdgb_ctx* c, int cg, const double* u, double* r, c
   switch (c->N) {
 #define HDGB_CASE(n)                                                             \
   case n:                                                                        \
-    return cg ? fx_launch<n, FX_POST, 1>(c, a, MS, w, n, s) : fx_launch<n, FX_POST, 0>(c, a, MS, w, n, s);
+    return cg ? fx_launch<n, FX_POST, 1>(c, a, MS, w, n, s, 1) : fx_launch<n, FX_POST, 0>(c, a, MS, w, n, s, 1);
     HDGB_CASE(2) HDGB_CASE(3) HDGB_CASE(4) HDGB_CASE(5) HDGB_CASE(6) HDGB_CASE(7) HDGB_CASE(8) HDGB_CASE(9)
     HDGB_CASE(10) HDGB_CASE(11) HDGB_CASE(12) HDGB_CASE(13) HDGB_CASE(14) HDGB_CASE(15) HDGB_CASE(16)
     HDGB_CASE(17)
@@ -931,7 +1034,7 @@ static cudaError_t face_n(hdgb_ctx* c, int op, int prec, const FaceArgs& a, cuda
         b.in = a.r;
         TabOff to;
         to.set(N);
-        return fx_launch<N, FX_UPDATE, 1>(c, b, c->h_tab.data() + to.St, c->h_tab.data() + to.S, N * N, s);
+        return fx_launch<N, FX_UPDATE, 1>(c, b, c->h_tab.data() + to.St, c->h_tab.data() + to.S, N * N, s, 1);
       }
       if (c->pupd_x) return pw_prec<N, PW_UPDATE, true, true>(c, prec, a, s);  // x update deferred
       if ((e = pw_prec<N, PW_UPDATE, true>(c, prec, a, s)) != cudaSuccess) return e;
@@ -969,8 +1072,8 @@ cudaError_t launch_face_transform_pupd(hdgb_ctx* c, const double* A_host, const 
   switch (c->N) {
 #define HDGB_CASE(n) \
   case n:            \
-    return a.x ? fx_launch<n, FX_TRANSFORM, 2>(c, a, A_host, nullptr, 0, s) \
-               : fx_launch<n, FX_TRANSFORM, 1>(c, a, A_host, nullptr, 0, s);
+    return a.x ? fx_launch<n, FX_TRANSFORM, 2>(c, a, A_host, nullptr, 0, s, 1) \
+               : fx_launch<n, FX_TRANSFORM, 1>(c, a, A_host, nullptr, 0, s, 1);
     HDGB_CASE(2) HDGB_CASE(3) HDGB_CASE(4) HDGB_CASE(5) HDGB_CASE(6) HDGB_CASE(7) HDGB_CASE(8) HDGB_CASE(9)
     HDGB_CASE(10) HDGB_CASE(11) HDGB_CASE(12) HDGB_CASE(13) HDGB_CASE(14) HDGB_CASE(15) HDGB_CASE(16)
     HDGB_CASE(17)
@@ -979,9 +1082,11 @@ cudaError_t launch_face_transform_pupd(hdgb_ctx* c, const double* A_host, const 
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_face_transform(hdgb_ctx* c, const double* A_host, const double* in, double* out, cudaStream_t s) {
+cudaError_t launch_face_transform(hdgb_ctx* c, const double* A_host, const double* in, double* out, cudaStream_t s,
+                                  int fold) {
   FaceArgs a = base_args(c, HDGB_PREC_NONE);
   a.A = A_host;
+  a.fold = fold;  // only the context's own T (plain pre-transform) is folded; user matrices are not
   a.in = in;
   a.out = out;
   return face_any(c, OP_TRANSFORM, HDGB_PREC_NONE, a, s);

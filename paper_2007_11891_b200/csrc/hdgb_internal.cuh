@@ -149,6 +149,7 @@ struct FaceArgs {
   CGState* st;
   cudaGraphConditionalHandle loop;  // PCG graph: the x, r update ends the loop once done
   int loop_on;
+  int fold;              // FX_TRANSFORM: A is the context's T (parity-folded products allowed)
 };
 
 // ---------------------------------------------------------------- deterministic reductions
@@ -305,6 +306,10 @@ struct hdgb_ctx {
     int64_t launches = 0;
   } io_graph[2][2];
   int64_t launches = 0;
+  // eigenvector parities of S (bit a: S[N-1-i][a] = +S[i][a]) and whether the face kernels may
+  // use the parity-folded 1D products (HDGB_FOLD=0 disables)
+  uint32_t sig = 0;
+  int fold_ok = 0;
   // L2 working-set target of one z-slab of the colour passes; 0 = one slab.  Slabbing cuts
   // HBM traffic (pass-0 partials stay in L2) but multiplies launches; while the element
   // kernels are issue-bound the single slab is faster (HDGB_SLAB_MB overrides).
@@ -317,7 +322,8 @@ int cuda_fail(cudaError_t e, const char* what);
 
 // launchers (defined per translation unit)
 cudaError_t launch_op(hdgb_ctx* c, int variant, int mode, const double* u, double* r, cudaStream_t s);
-cudaError_t launch_face_transform(hdgb_ctx* c, const double* A_host, const double* in, double* out, cudaStream_t s);
+cudaError_t launch_face_transform(hdgb_ctx* c, const double* A_host, const double* in, double* out, cudaStream_t s,
+                                  int fold = 0);
 cudaError_t launch_plain_post(hdgb_ctx* c, int cg, const double* u, double* r, cudaStream_t s);
 cudaError_t launch_face_transform_pupd(hdgb_ctx* c, const double* A_host, const double* z, double* p, double* out,
                                        cudaStream_t s);

@@ -499,7 +499,7 @@ static cudaError_t launch_t(hdgb_ctx* c, const double* u, double* r, cudaStream_
     cudaError_t e = (MODE & 1) && c->pupd_z
                         ? launch_face_transform_pupd(c, c->h_tab.data() + to.T, c->pupd_z, const_cast<double*>(u),
                                                      c->d_hat, s)
-                        : launch_face_transform(c, c->h_tab.data() + to.T, u, c->d_hat, s);
+                        : launch_face_transform(c, c->h_tab.data() + to.T, u, c->d_hat, s, 1);
     if (e != cudaSuccess) return e;
     a.u = c->d_hat;
   }

@@ -455,3 +455,35 @@ def test_full_size_operator_properties(p, m):
         del kx, ky, kxy
     del dc, ctx, x, y
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 7, 8, 11, 12, 16])
+@pytest.mark.parametrize("fold", ["0", "1"])
+def test_parity_folded_face_products(p, fold, monkeypatch):
+    """Face kernels with and without the parity-folded 1D products (even/odd eigenvectors of S),
+    forced at every degree: plain operator, block preconditioner and the fused block PCG against
+    the oracle."""
+    from paper_2007_11891_b200.operator import DeviceContext
+
+    monkeypatch.setenv("HDGB_FOLD", fold)
+    monkeypatch.setenv("HDGB_FOLD_NMIN", "2")
+    bc = ("neumann", "dirichlet", "dirichlet", "neumann", "dirichlet", "neumann")
+    lo, hi = (0.0, 0.0, 0.0), (1.5, 1.0, 1.0)
+    mesh = hb.Mesh((3, 2, 2), lo, hi, bc)
+    basis = hb.Basis1D(p, 0.6)
+    dc = DeviceContext(basis, mesh, 0.4)
+    octx = O.context(O.basis_1d(p, 0.6), O.Grid.uniform(mesh.n, lo, hi, bc), 0.4)
+    u = np.random.default_rng(p).uniform(-1, 1, mesh.n_all(p))
+    assert relerr(dc.apply(_dev(u), 0).cpu().numpy(), O.apply_op(octx, u, False)) < TOL
+    y = O.face_selfcoupling(octx)
+    assert relerr(dc.prec(_dev(u), 1).cpu().numpy(), O.block_prec_apply(octx, y, u)) < TOL
+    F = dc.unpack(_dev(np.random.default_rng(p + 1).uniform(-1, 1, dc.n_unknown)))
+    x = torch.zeros_like(F)
+    it, rel, conv = dc.pcg(0, 1, F, x, 1e-10, 0.0, 500)
+    grid, n = octx["grid"], octx["n"]
+    Fp = dc.pack(F).cpu().numpy()
+    xo, ito, _, _ = O.pcg(lambda v: O.apply_op_packed(octx, v),
+                          lambda r: O.pack(grid, n, O.block_prec_apply(octx, y, O.unpack(grid, n, r))), Fp,
+                          np.zeros_like(Fp))
+    assert conv and abs(it - ito) <= 1, (it, ito)
+    assert relerr(dc.pack(x).cpu().numpy(), xo) < 1e-9
