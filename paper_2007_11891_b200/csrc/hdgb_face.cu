@@ -170,8 +170,10 @@ struct FxCfg {
 #define HDGB_FX_WIDE_N 13
 #endif
   // warps per CTA
+  // (the PCG variants at N = 17 stay narrow: block PCG p = 16 1396 -> 1196 us/iter)
   static constexpr int WARPS =
-      (N >= HDGB_FX_WIDE_N && (FK == FX_TRANSFORM || FK == FX_POST)) ? 2 * HDGB_FX_WARPS : HDGB_FX_WARPS;
+      (N >= HDGB_FX_WIDE_N && (FK == FX_TRANSFORM || FK == FX_POST) && !(CG && N >= 17)) ? 2 * HDGB_FX_WARPS
+                                                                                         : HDGB_FX_WARPS;
   static constexpr int NG = WARPS / GW;              // independent groups per CTA
   static constexpr int NT = 32 * WARPS;
   static constexpr int NP = 17;                      // exchange row pitch, = 1 (mod 16)
