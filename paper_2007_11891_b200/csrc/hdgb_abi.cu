@@ -546,7 +546,6 @@ int hdgb_vec_axpby(int64_t n, double a, const double* x, double b, const double*
 #endif
 static cudaError_t enqueue_iteration(hdgb_ctx* c, int variant, int prec, cudaGraphConditionalHandle h, int has_loop) {
   double* v = c->d_vec;
-  const int64_t n = c->n_all;
   cudaError_t e;
   // p = z + beta p fused into the operator (beta = 0 before the first iteration, when p = z
   // already): the plain pre-transform, or the transformed colour passes; w = K p with <p, w>

@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t sBar[C::NG][S];
   __shared__ double sWq[N];  // FX_POST: quadrature weights (dynamic index: keep out of the constant bank)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const int grp = warp / GW, gl = threadIdx.x - grp * GT;  // group and thread within it
   const int f = gl / N, l = gl - (gl / N) * N;
   const bool on_lane = f < FPW;
@@ -1124,7 +1124,6 @@ enum { V_X = 0, V_R = 1, V_Z = 2, V_P = 3, V_W = 4, V_F = 5 };
 cudaError_t launch_cg_init(hdgb_ctx* c, int kind, cudaStream_t s) {
   FaceArgs a = base_args(c, kind);
   double* v = c->d_vec;
-  const int64_t n = c->n_all;
   a.in = v + V_F * c->vstride;
   a.w = v + V_W * c->vstride;
   a.r = v + V_R * c->vstride;
@@ -1138,7 +1137,6 @@ cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s, cudaGraphCon
   a.loop = loop;
   a.loop_on = loop_on;
   double* v = c->d_vec;
-  const int64_t n = c->n_all;
   a.x = v + V_X * c->vstride;
   a.p = v + V_P * c->vstride;
   a.r = v + V_R * c->vstride;
