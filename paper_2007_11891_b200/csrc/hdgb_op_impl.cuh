@@ -104,7 +104,7 @@ struct OpVCfg {
   static constexpr int MINB = HDGB_OPV_MINB;
 #else
   // register budget (CTAs per SM): measured on the config-3 sweep (p = 2..16)
-  static constexpr int MINB = NT > 256 ? 2 : (N <= 7 ? 3 : (N <= 11 ? 2 : 3));
+  static constexpr int MINB = NT > 256 ? 2 : (N <= 5 ? 3 : (N <= 11 ? 2 : 3));  // N = 6, 7: 2 (p = 5: 216 -> 210 us)
 #endif
   // staging of the six faces: bulk async copies (TMA unit, one mbarrier per buffer) for
   // N >= HDGB_OPV_TMA_NMIN, per-thread cp.async below.  A face of odd NQ starts on an 8-byte
