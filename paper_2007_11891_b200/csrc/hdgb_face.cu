@@ -199,7 +199,9 @@ struct FxCfg {
   static constexpr int S = (FK == FX_TRANSFORM && CG && HDGB_FXT_S) ? HDGB_FXT_S
                            : (FK == FX_UPDATE && CG && HDGB_FXU_S) ? HDGB_FXU_S
                            : (FK == FX_POST && CG && HDGB_FXPC_S) ? HDGB_FXPC_S
-                                                                   : (N <= 11 ? 3 : 2);  // ring stages per group
+                                                                   : 2;  // ring stages per group
+  // (2 stages for every N since the folded/unfolded product code lowered the register use: config-2
+  // plain apply 34.8 -> 32.8 us, p = 8 409.6 -> 395.3 us against 3 stages for N <= 11)
 #endif
   static constexpr int EPT = (FPW * N2 + GT - 1) / GT;  // epilogue values per thread
   // FX_POST stages u next to G with the same bulk copies for N <= 11 (measured: p = 8 plain
