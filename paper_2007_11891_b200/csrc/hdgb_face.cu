@@ -244,7 +244,12 @@ struct FxCfg {
 #ifndef HDGB_FXPC_MINB
 #define HDGB_FXPC_MINB 2
 #endif
-  static constexpr int MINB = ((FK == FX_POST && !CG && OPS == 2) || (FK == FX_PREC && N >= 8)) ? 3
+#ifndef HDGB_FX_MINB4_N
+#define HDGB_FX_MINB4_N 11
+#endif
+  // N <= 11: 4 CTAs/SM for every kind (block PCG p = 4 744 -> 722, p = 8 772 -> 761, p = 10 789 -> 779 us/iter)
+  static constexpr int MINB = N <= HDGB_FX_MINB4_N ? 4
+                              : ((FK == FX_POST && !CG && OPS == 2) || (FK == FX_PREC && N >= 8)) ? 3
                               : (FK == FX_UPDATE ? HDGB_FXU_MINB
                                                  : (FK == FX_TRANSFORM && CG ? HDGB_FXT_MINB
                                                                              : (FK == FX_POST && CG ? HDGB_FXPC_MINB : 2)));
