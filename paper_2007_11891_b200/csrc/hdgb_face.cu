@@ -30,8 +30,14 @@ __device__ __forceinline__ void cp_async8f(double* smem_dst, const double* gsrc)
 
 // ================================================================ pointwise kernels
 enum { PW_PREC = 0, PW_INIT = 1, PW_UPDATE = 2 };
-constexpr int PW_U = 4;       // elements per thread per sweep
-constexpr int PW_GRID = 1184; // fixed grid (8 CTAs x 148 SMs)
+#ifndef HDGB_PW_U
+#define HDGB_PW_U 4
+#endif
+#ifndef HDGB_PW_GRID
+#define HDGB_PW_GRID 1184
+#endif
+constexpr int PW_U = HDGB_PW_U;        // elements per thread per sweep
+constexpr int PW_GRID = HDGB_PW_GRID;  // fixed grid (8 CTAs x 148 SMs)
 
 // NOX (PCG with the x update deferred into the next direction update): r -= alpha w only
 template <int N, int PREC, int FK, bool WITHZ, bool NOX = false>
