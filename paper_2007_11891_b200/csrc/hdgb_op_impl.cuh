@@ -98,13 +98,26 @@ __device__ __forceinline__ void elem_alpha(const OpArgs& a, const int* c, double
 template <int N>
 struct OpVCfg {
   static constexpr int NQ = N * N;                      // threads (face positions) per element
-  static constexpr int G = NQ >= 256 ? 1 : 256 / NQ;    // elements per CTA
+#ifndef HDGB_OPV_THREADS
+#define HDGB_OPV_THREADS 256
+#endif
+#ifndef HDGB_OPV_SMALL_N0
+#define HDGB_OPV_SMALL_N0 10
+#endif
+#ifndef HDGB_OPV_SMALL_N1
+#define HDGB_OPV_SMALL_N1 13
+#endif
+  // N in [SMALL_N0, SMALL_N1]: one element per 128-thread CTA and 4 CTAs per SM (transformed
+  // apply p = 9..12: 271 -> 255, 267 -> 251, 296 -> 281, 314 -> 296 us; slower from N = 14 up)
+  static constexpr bool SMALL = N >= HDGB_OPV_SMALL_N0 && N <= HDGB_OPV_SMALL_N1;
+  static constexpr int THREADS = SMALL ? 128 : HDGB_OPV_THREADS;
+  static constexpr int G = NQ >= THREADS ? 1 : THREADS / NQ;  // elements per CTA
   static constexpr int NT = (G * NQ + 31) / 32 * 32;    // threads per CTA
 #ifdef HDGB_OPV_MINB
   static constexpr int MINB = HDGB_OPV_MINB;
 #else
   // register budget (CTAs per SM): measured on the config-3 sweep (p = 2..16)
-  static constexpr int MINB = NT > 256 ? 2 : (N <= 5 ? 3 : (N <= 11 ? 2 : 3));  // N = 6, 7: 2 (p = 5: 216 -> 210 us)
+  static constexpr int MINB = SMALL ? 4 : (NT > 256 ? 2 : (N <= 5 ? 3 : (N <= 11 ? 2 : 3)));  // N = 6, 7: 2 (p = 5: 216 -> 210 us)
 #endif
   // staging of the six faces: bulk async copies (TMA unit, one mbarrier per buffer) for
   // N >= HDGB_OPV_TMA_NMIN, per-thread cp.async below.  A face of odd NQ starts on an 8-byte
