@@ -105,10 +105,11 @@ struct OpVCfg {
 #define HDGB_OPV_SMALL_N0 10
 #endif
 #ifndef HDGB_OPV_SMALL_N1
-#define HDGB_OPV_SMALL_N1 13
+#define HDGB_OPV_SMALL_N1 12
 #endif
   // N in [SMALL_N0, SMALL_N1]: one element per 128-thread CTA and 4 CTAs per SM (transformed
-  // apply p = 9..12: 271 -> 255, 267 -> 251, 296 -> 281, 314 -> 296 us; slower from N = 14 up)
+  // apply p = 9..11: 271 -> 255, 267 -> 251, 296 -> 281 us, transformed PCG p = 10 549 -> 523
+  // us/iter; at N = 13 the fused-update PCG variant lost 614 -> 676 us/iter, slower N >= 14)
   static constexpr bool SMALL = N >= HDGB_OPV_SMALL_N0 && N <= HDGB_OPV_SMALL_N1;
   static constexpr int THREADS = SMALL ? 128 : HDGB_OPV_THREADS;
   static constexpr int G = NQ >= THREADS ? 1 : THREADS / NQ;  // elements per CTA
