@@ -110,7 +110,9 @@ struct OpVCfg {
   // N in [SMALL_N0, SMALL_N1]: one element per 128-thread CTA and 4 CTAs per SM (transformed
   // apply p = 9..11: 271 -> 255, 267 -> 251, 296 -> 281 us, transformed PCG p = 10 549 -> 523
   // us/iter; at N = 13 the fused-update PCG variant lost 614 -> 676 us/iter, slower N >= 14)
-  static constexpr bool SMALL = N >= HDGB_OPV_SMALL_N0 && N <= HDGB_OPV_SMALL_N1;
+  // (also N = 8: p = 7 transformed PCG 509 -> 494 us/iter; not N = 9, where 3 elements fill a
+  // 256-thread CTA: p = 8 transformed apply 257 -> 298 us)
+  static constexpr bool SMALL = (N >= HDGB_OPV_SMALL_N0 && N <= HDGB_OPV_SMALL_N1) || N == 8;
   static constexpr int THREADS = SMALL ? 128 : HDGB_OPV_THREADS;
   static constexpr int G = NQ >= THREADS ? 1 : THREADS / NQ;  // elements per CTA
   static constexpr int NT = (G * NQ + 31) / 32 * 32;    // threads per CTA
