@@ -95,7 +95,8 @@ __device__ __forceinline__ void elem_alpha(const OpArgs& a, const int* c, double
   }
 }
 
-template <int N>
+// PU: the colour-0 pass with the fused PCG direction update (MODE bits 0 and 3)
+template <int N, bool PU = false>
 struct OpVCfg {
   static constexpr int NQ = N * N;                      // threads (face positions) per element
 #ifndef HDGB_OPV_THREADS
@@ -105,14 +106,16 @@ struct OpVCfg {
 #define HDGB_OPV_SMALL_N0 10
 #endif
 #ifndef HDGB_OPV_SMALL_N1
-#define HDGB_OPV_SMALL_N1 12
+#define HDGB_OPV_SMALL_N1 13
 #endif
   // N in [SMALL_N0, SMALL_N1]: one element per 128-thread CTA and 4 CTAs per SM (transformed
   // apply p = 9..11: 271 -> 255, 267 -> 251, 296 -> 281 us, transformed PCG p = 10 549 -> 523
   // us/iter; at N = 13 the fused-update PCG variant lost 614 -> 676 us/iter, slower N >= 14)
   // (also N = 8: p = 7 transformed PCG 509 -> 494 us/iter; not N = 9, where 3 elements fill a
   // 256-thread CTA: p = 8 transformed apply 257 -> 298 us)
-  static constexpr bool SMALL = (N >= HDGB_OPV_SMALL_N0 && N <= HDGB_OPV_SMALL_N1) || N == 8;
+  // (not the fused-update colour-0 pass at N = 13: its staging measured slower
+  // in the small shape: transformed PCG p = 12 614 -> 676 us/iter)
+  static constexpr bool SMALL = ((N >= HDGB_OPV_SMALL_N0 && N <= HDGB_OPV_SMALL_N1) || N == 8) && !(PU && N == 13);
   static constexpr int THREADS = SMALL ? 128 : HDGB_OPV_THREADS;
   static constexpr int G = NQ >= THREADS ? 1 : THREADS / NQ;  // elements per CTA
   static constexpr int NT = (G * NQ + 31) / 32 * 32;    // threads per CTA
@@ -177,9 +180,10 @@ struct ElemInfo {
 // MODE bit 0: CG (Dirichlet rows -> 0, <p, w> and alpha from a fixed-order reduction at the end); bit 1: non-uniform grid (per-element
 // metric terms and dz_inv); bit 2: "g only" (plain core: emit the eigen-space sum of g only).
 template <int N, int MODE, int COLOR>
-__global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(const OpArgs a, int64_t t0, int64_t t1,
+__global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
+                                  OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::MINB) opV_kernel(const OpArgs a, int64_t t0, int64_t t1,
                                                           const __grid_constant__ OpVConst<N> K) {
-  using C = OpVCfg<N>;
+  using C = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>;
   constexpr int NQ = C::NQ, G = C::G, FS = C::FS, VS = C::VS;
   constexpr bool UNI = !(MODE & 2), CG = MODE & 1, GONLY = MODE & 4;
   // bit 3 (CG, colour 0 only): p = z + beta p (solver.py:320) fused into the staging of this
@@ -469,7 +473,7 @@ __global__ void __launch_bounds__(OpVCfg<N>::NT, OpVCfg<N>::MINB) opV_kernel(con
 
 template <int N, int MODE, int COLOR>
 static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_t t1, cudaStream_t s) {
-  using Cf = OpVCfg<N>;
+  using Cf = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>;
   const size_t smem = sizeof(double) * (size_t)Cf::smem_doubles((MODE & 9) == 9 && COLOR == 0);
   auto kern = opV_kernel<N, MODE, COLOR>;
   static int cache[16] = {0};
