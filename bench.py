@@ -36,6 +36,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CFG = dict(n_el=(16, 16, 16), p=8, lam=1.0, tau=25.0)
+METRIC = "FP64 trace-DOF/s per operator apply (plain Alg. 2, hdg_op_3d)"
 L2_FLUSH_BYTES = 512 << 20
 
 
@@ -107,6 +108,32 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def _gpu_affinity(device):
+    """Pin this process to the GPU's NUMA-local CPUs (NVML ideal affinity) before any pinned
+    host buffer is allocated, so page-locked staging is first-touched NUMA-local to the GPU."""
+    rec = {"applied": False, "numa_node": None, "cpus": None}
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        ncpu = os.cpu_count() or 1
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (ncpu + 63) // 64)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1 and w * 64 + b < ncpu}
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            rec.update(applied=True, cpus=len(cpus))
+        bus = pynvml.nvmlDeviceGetPciInfo(h).busId
+        bus = bus.decode() if isinstance(bus, bytes) else bus
+        path = f"/sys/bus/pci/devices/{bus.lower()[-12:]}/numa_node"
+        if os.path.exists(path):
+            with open(path) as fh:
+                rec["numa_node"] = int(fh.read().strip())
+    except Exception as exc:  # keep the bench running without NVML
+        rec["error"] = f"{type(exc).__name__}: {exc}"
+    return rec
+
+
 def build_problem(rank=0, world=1):
     import paper_2007_11891_b200 as hb
 
@@ -132,31 +159,77 @@ def _sin_rhs(hb, mesh, ctx):
     return hb.pack_unknowns(hb.build_rhs(f, None, None, ctx))
 
 
-def cpu_oracle_apply(seconds=10.0, threads=1, steps=None, warmup=1):
-    """Time the CPU oracle (numpy restatement of the reference apply) on config 2."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+WORKLOAD = ("BASELINE configs[1]: 16^3 uniform elements, p=8 (GLL), lambda=1, unit cube, homogeneous "
+            "Dirichlet, tau=25 ('element'); seeded uniform[-1,1] packed trace vector (rng(1))")
+
+
+def _reference_module():
+    """The UNMODIFIED reference package (hdgbox), installed per pod under baseline/_ref/ (gitignored)."""
+    if not os.path.isdir(os.path.join(REF_DIR, "hdgbox")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import hdgbox
+
+    return hdgbox
+
+
+def cpu_apply(seconds=10.0, threads=1, steps=None, warmup=1):
+    """Time the reference's own apply_K closure on config 2 on the host cores.
+
+    apply_K(v) = pack_unknowns(hdg_op_3d(unpack_unknowns(v, mesh, p), ctx)) as solve() builds it
+    (hdgbox/solver.py:348-349), under threadpool_limits(threads) like harness.run_experiment
+    (harness.py:251-263).  Falls back to the numpy oracle port (oracle/hdg_oracle.py) when the
+    reference is not installed.  Returns (N, times, kind)."""
     from threadpoolctl import threadpool_limits
 
-    from oracle import hdg_oracle as O
+    H = _reference_module()
+    p = CFG["p"]
+    if H is not None:
+        from hdgbox.mesh import pack_unknowns, unpack_unknowns
 
-    octx = O.problem(CFG["n_el"], CFG["p"], CFG["lam"], tau=CFG["tau"])
-    grid, n = octx["grid"], octx["n"]
-    N = grid.n_unknowns(n)
+        mesh = H.Mesh(CFG["n_el"], (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), "dirichlet")
+        ctx = H.make_context(mesh, p, H.SolverConfig(lam=CFG["lam"], tau=CFG["tau"]))
+        N = mesh.n_trace_unknowns(p)
+
+        def apply_K(v):
+            return pack_unknowns(H.hdg_op_3d(unpack_unknowns(v, mesh, p), ctx))
+
+        kind = "reference"
+    else:
+        from oracle import hdg_oracle as O
+
+        octx = O.problem(CFG["n_el"], p, CFG["lam"], tau=CFG["tau"])
+        N = octx["grid"].n_unknowns(octx["n"])
+
+        def apply_K(v):
+            return O.apply_op_packed(octx, v)
+
+        kind = "port"
     v = np.random.default_rng(1).uniform(-1.0, 1.0, N)
     times = []
     with threadpool_limits(limits=threads):
         for _ in range(max(warmup, 0)):
-            O.apply_op_packed(octx, v)
+            apply_K(v)
         t_start = time.perf_counter()
         while True:
             t0 = time.perf_counter()
-            O.apply_op_packed(octx, v)
+            apply_K(v)
             times.append(time.perf_counter() - t0)
             if steps is not None:
                 if len(times) >= steps:
                     break
             elif time.perf_counter() - t_start >= seconds and len(times) >= 3:
                 break
-    return N, times
+    return N, times, kind
+
+
+def _cpu_sample(kind, times, threads):
+    what = ("hdgbox (unmodified reference, baseline/_ref) apply_K = pack o hdg_op_3d o unpack"
+            if kind == "reference" else "numpy oracle port of hdgbox hdg_op_3d (reference not installed)")
+    return (f"{len(times)} applies of config 2 by {what}, threadpool_limits({threads}), median "
+            f"{statistics.median(times) * 1e3:.1f} ms; host {os.cpu_count()} cores")
 
 
 def run_reference(args):
@@ -164,19 +237,17 @@ def run_reference(args):
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    N, times = cpu_oracle_apply(threads=cores, steps=args.steps, warmup=args.warmup)
+    N, times, kind = cpu_apply(threads=cores, steps=args.steps, warmup=args.warmup)
     t = statistics.median(times)
     val = N / t
     line = {
-        "metric": "FP64 trace-DOF/s per operator apply (plain Alg. 2, hdg_op_3d)",
+        "metric": METRIC,
         "value": val, "unit": "trace-DOF/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1] trace vector)",
-        "config": {"workload": "BASELINE configs[1]: 16^3 elements, p=8, lambda=1, unit cube, Dirichlet",
-                   "trace_unknowns": N},
-        "cpu_baseline": {"value": val, "unit": "trace-DOF/s", "cores": cores, "kind": "port",
-                         "sample": f"{len(times)} oracle applies of config 2 (numpy restatement of "
-                                   f"hdgbox hdg_op_3d; BLAS threads={cores})"},
+        "config": {"workload": WORKLOAD, "trace_unknowns": N},
+        "cpu_baseline": {"value": val, "unit": "trace-DOF/s", "cores": cores, "kind": kind,
+                         "sample": _cpu_sample(kind, times, cores)},
         "e2e": {"value": val, "unit": "trace-DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -230,7 +301,7 @@ def _large_point(hb, p, m, lam, flush, stream, hbm, fp64_peak, reps=10, mesh=Non
             b.synchronize()
             ts.append(a.elapsed_time(b) * 1e-3)
         t = statistics.median(ts)
-        ent = {"us": t * 1e6, "trace_dof_per_s": N / t, "hbm_frac": 16 * N_all / t / 1e9 / hbm}
+        ent = {"us": t * 1e6, "trace_dof_per_s": N / t, "hbm_frac": 16 * N / t / 1e9 / hbm}
         if name == "plain":
             ent["fp64_frac"] = mesh.n_elements * (73 * n ** 3 + 12 * n ** 2) / t / 1e12 / fp64_peak
         if name == "transformed":
@@ -259,7 +330,7 @@ def _large_point(hb, p, m, lam, flush, stream, hbm, fp64_peak, reps=10, mesh=Non
             ts.append(a.elapsed_time(b) * 1e-3)
         t_it = statistics.median(ts) / max(it, 1)
         out[name] = {"us_per_iter": t_it * 1e6, "ps_per_unknown_per_iter": t_it / N * 1e12,
-                     "hbm_frac_of_96B_per_unknown": 96 * N_all / t_it / 1e9 / hbm, "iterations": it}
+                     "hbm_frac_of_96B_per_unknown": 96 * N / t_it / 1e9 / hbm, "iterations": it}
     del dc, ctx, u, r
     torch.cuda.empty_cache()
     return out
@@ -404,6 +475,7 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    affinity = _gpu_affinity(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     p, n = CFG["p"], CFG["p"] + 1
@@ -478,7 +550,7 @@ def run_ours(args):
     ms_t, _ = _timed_apply(dc, u, r, 1, steps, 2, flush, stream)
     t_tr = statistics.fmean(ms_t) * 1e-3
     hbm, peak_kind = _peaks()
-    alg_bytes = 16 * N_all  # read u once + write r once, all faces (16 B per trace unknown)
+    alg_bytes = 16 * N  # read u once + write r once (16 B per trace unknown)
     # dominant kernel: the element kernel pair (opV colour passes 0 + 1).  The transformed apply
     # (Alg. 3) is exactly that pair; the plain apply wraps it in two face-block launches.
     achieved = alg_bytes / t_tr / 1e9
@@ -515,6 +587,24 @@ def run_ours(args):
         b.synchronize()
         e2e_ms.append(a.elapsed_time(b))
     t_e2e = statistics.median(e2e_ms) * 1e-3
+    # the two PCIe copies alone (same pinned buffers, same sizes)
+    d_in = torch.empty(n_e2e, dtype=torch.float64, device="cuda")
+    h2d_ms, d2h_ms = [], []
+    for _ in range(max(steps, 5)):
+        a, b, c2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record(stream)
+        d_in.copy_(h_u, non_blocking=True)
+        b.record(stream)
+        h_r.copy_(d_in, non_blocking=True)
+        c2.record(stream)
+        c2.synchronize()
+        h2d_ms.append(a.elapsed_time(b))
+        d2h_ms.append(b.elapsed_time(c2))
+    del d_in
+    pcie = {"h2d_ms": statistics.median(h2d_ms), "d2h_ms": statistics.median(d2h_ms),
+            "h2d_gbs": 8 * n_e2e / statistics.median(h2d_ms) / 1e6, "d2h_gbs": 8 * n_e2e / statistics.median(d2h_ms) / 1e6,
+            "affinity": affinity}
+    e2e_step()  # h_r holds the apply again (checked below)
     apply_step(0)
     ref_e2e = dc.pack(r).cpu().numpy() if world == 1 else r.cpu().numpy()
     assert np.array_equal(hr, ref_e2e), "e2e result differs from the device-resident apply"
@@ -544,7 +634,7 @@ def run_ours(args):
         cg = {"preconditioner": "block (Alg. 4)", "iterations": it, "converged": conv, "relres": rel,
               "solve_ms": t_cg * 1e3, "us_per_unknown_per_iter": t_cg / it / N * 1e6,
               "ms_per_iter": t_cg / it * 1e3,
-              "hbm_frac_of_96B_per_unknown": (96 * N_all / (t_cg / it) / 1e9) / hbm,
+              "hbm_frac_of_96B_per_unknown": (96 * N / (t_cg / it) / 1e9) / hbm,
               "note": "whole solve incl. setup kernels, one CUDA graph with device-side while loop; "
                       "config-2 vectors are L2-resident during the solve"}
         # transformed pipeline (solve_transformed, solver.py:372-410): F_hat = (S^T (x) S^T) F,
@@ -640,29 +730,80 @@ def run_ours(args):
     # ---- CPU oracle on this host (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        Nc, times = cpu_oracle_apply(seconds=args.cpu_seconds, threads=1)
+        Nc, times, kind = cpu_apply(seconds=args.cpu_seconds, threads=1)
         tc = statistics.median(times)
-        cpu = {"value": Nc / tc, "unit": "trace-DOF/s", "cores": 1, "kind": "port",
-               "sample": f"{len(times)} applies of config 2 by the numpy oracle (restatement of hdgbox "
-                         f"hdg_op_3d), threadpool_limits(1), median {tc * 1e3:.1f} ms; host "
-                         f"{os.cpu_count()} cores"}
+        cpu = {"value": Nc / tc, "unit": "trace-DOF/s", "cores": 1, "kind": kind,
+               "sample": _cpu_sample(kind, times, 1)}
+
+    # ---- roofline of the dominant kernel: the element-kernel pair (opV colour passes 0 + 1 = one
+    # transformed apply, the core of the plain apply) on an HBM-scale grid, config 3 at p = 8
+    # (44^3, 2.0e7 unknowns, 160 MB per vector >> 126 MB L2), timed above with CUDA events on the
+    # launching stream; 16 B per trace unknown.  Config 2 (8 MB vectors, L2-resident,
+    # 2.3 waves of CTAs) is reported beside it.
+    cfg2_roof = {"workload": "config 2 (16^3, p=8)", "pair_ms": t_tr * 1e3,
+                 "pair_frac": (alg_bytes / t_tr / 1e9) / hbm, "plain_apply_ms": t_k * 1e3,
+                 "plain_apply_frac": (alg_bytes / t_k / 1e9) / hbm,
+                 "traffic": (traffic or {}).get("config2", {}).get("bytes_per_launch")}
+    c3 = large.get("config3_p8")
+    if c3 is not None:
+        N3 = c3["trace_unknowns"]
+        t_pair, t_plain3 = c3["transformed"]["us"] * 1e-6, c3["plain"]["us"] * 1e-6
+        ach = 16 * N3 / t_pair / 1e9
+        roofline = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                    "traffic": (traffic or {}).get("config3_p8", {}).get("bytes_per_launch"),
+                    "kernel": "opV_kernel<9> element kernel pair (colour pass 0 + 1 = one transformed apply)",
+                    "workload": "config 3 at p=8: 44^3 elements, lambda=0, seed 8", "kernel_ms": t_pair * 1e3,
+                    "algorithmic_bytes_per_launch": 16 * N3, "plain_apply_ms": t_plain3 * 1e3,
+                    "plain_apply_frac": 16 * N3 / t_plain3 / 1e9 / hbm, "peak_kind": peak_kind,
+                    "note": "'launch' = both colour passes; 16 B per trace unknown (read u, write r)",
+                    "config2": cfg2_roof}
+    else:
+        roofline = {"bound": "hbm", "achieved": alg_bytes / t_tr / 1e9, "peak": hbm, "unit": "GB/s",
+                    "frac": (alg_bytes / t_tr / 1e9) / hbm, "traffic": cfg2_roof["traffic"],
+                    "kernel": "opV_kernel<9> element kernel pair (colour pass 0 + 1 = one transformed apply)",
+                    "workload": "config 2 (L2-resident: not an HBM-scale point)", "kernel_ms": t_tr * 1e3,
+                    "algorithmic_bytes_per_launch": alg_bytes, "plain_apply_frac": cfg2_roof["plain_apply_frac"],
+                    "peak_kind": peak_kind}
+
+    # ---- roofline of the dominant kernel: the element-kernel pair (opV colour passes 0 + 1 = one
+    # transformed apply, the core of the plain apply) on an HBM-scale grid, config 3 at p = 8
+    # (44^3, 2.0e7 unknowns, 160 MB per vector >> 126 MB L2), timed above with CUDA events on the
+    # launching stream; 16 B per trace unknown.  Config 2 (8 MB vectors, L2-resident,
+    # 2.3 waves of CTAs) is reported beside it.
+    cfg2_roof = {"workload": "config 2 (16^3, p=8)", "pair_ms": t_tr * 1e3,
+                 "pair_frac": (alg_bytes / t_tr / 1e9) / hbm, "plain_apply_ms": t_k * 1e3,
+                 "plain_apply_frac": (alg_bytes / t_k / 1e9) / hbm,
+                 "traffic": (traffic or {}).get("config2", {}).get("bytes_per_launch")}
+    c3 = large.get("config3_p8")
+    if c3 is not None:
+        N3 = c3["trace_unknowns"]
+        t_pair, t_plain3 = c3["transformed"]["us"] * 1e-6, c3["plain"]["us"] * 1e-6
+        ach = 16 * N3 / t_pair / 1e9
+        roofline = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                    "traffic": (traffic or {}).get("config3_p8", {}).get("bytes_per_launch"),
+                    "kernel": "opV_kernel<9> element kernel pair (colour pass 0 + 1 = one transformed apply)",
+                    "workload": "config 3 at p=8: 44^3 elements, lambda=0, seed 8", "kernel_ms": t_pair * 1e3,
+                    "algorithmic_bytes_per_launch": 16 * N3, "plain_apply_ms": t_plain3 * 1e3,
+                    "plain_apply_frac": 16 * N3 / t_plain3 / 1e9 / hbm, "peak_kind": peak_kind,
+                    "note": "'launch' = both colour passes; 16 B per trace unknown (read u, write r)",
+                    "config2": cfg2_roof}
+    else:
+        roofline = {"bound": "hbm", "achieved": alg_bytes / t_tr / 1e9, "peak": hbm, "unit": "GB/s",
+                    "frac": (alg_bytes / t_tr / 1e9) / hbm, "traffic": cfg2_roof["traffic"],
+                    "kernel": "opV_kernel<9> element kernel pair (colour pass 0 + 1 = one transformed apply)",
+                    "workload": "config 2 (L2-resident: not an HBM-scale point)", "kernel_ms": t_tr * 1e3,
+                    "algorithmic_bytes_per_launch": alg_bytes, "plain_apply_frac": cfg2_roof["plain_apply_frac"],
+                    "peak_kind": peak_kind}
 
     line = {
-        "metric": "FP64 trace-DOF/s per operator apply (plain Alg. 2, hdg_op_3d)",
+        "metric": METRIC,
         "value": value, "unit": "trace-DOF/s", "n_gpus": world, "steps": steps, "warmup": warm,
         "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded uniform[-1,1] trace vector; manufactured sin RHS for CG)",
-        "config": {"workload": "BASELINE configs[1]: 16^3 elements per GPU, p=8, lambda=1, unit cube per GPU, "
-                               "Dirichlet, tau=25 (element)",
+        "config": {"workload": WORKLOAD if world == 1 else WORKLOAD + f"; per GPU, x-slab of a [0,{world}]x[0,1]^2 box",
                    "trace_unknowns_per_gpu": N, "all_face_dofs_per_gpu": N_all,
                    "l2": "flushed before every timed step (512 MB write)", "parallelism": f"x-slab dp{world}"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": (traffic or {}).get("bytes_per_launch"),
-                     "kernel": "opV_kernel<9> element kernel, colour pass 0 + pass 1 (= one transformed apply)",
-                     "kernel_ms": t_tr * 1e3, "plain_apply_ms": t_k * 1e3,
-                     "plain_apply_hbm_frac": (alg_bytes / t_k / 1e9) / hbm,
-                     "algorithmic_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
-                     "note": "'launch' = both colour passes; 16 B per all-face DOF (read u, write r)"},
+        "roofline": roofline,
         "fp64": fp64,
         "transformed_apply": {"value": N / t_tr, "unit": "trace-DOF/s", "kernel_ms": t_tr * 1e3,
                               "hbm_frac": (alg_bytes / t_tr / 1e9) / hbm},
@@ -672,7 +813,8 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": {"value": world * N / t_e2e, "unit": "trace-DOF/s", "h2d_bytes_per_step": 8 * n_e2e,
                 "d2h_bytes_per_step": 8 * n_e2e, "ms_per_step": t_e2e * 1e3, "ms_min": min(e2e_ms),
-                "path": "hdgb_op_apply_host_packed (C ABI, pinned host buffers, packed unknown vectors)"},
+                "path": "hdgb_op_apply_host_packed (C ABI, pinned host buffers, packed unknown vectors)",
+                "copies": pcie, "floor_ms": pcie["h2d_ms"] + pcie["d2h_ms"]},
         "gpu_launches": launches,
         "clocks": clk.record(),
     }

@@ -94,6 +94,7 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
   hdgb_ctx* c = new hdgb_ctx();
   c->dev = d->device;
   if (const char* sb = getenv("HDGB_SLAB_MB")) c->slab_bytes = (int64_t)atof(sb) * (1LL << 20);
+  if (const char* gc = getenv("HDGB_GRID_CAP")) c->grid_cap = atoll(gc);
   if (cudaSetDevice(c->dev) != cudaSuccess) {
     delete c;
     return einval("invalid CUDA device");
@@ -145,6 +146,13 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
     }
   }
   c->uniform = uniform && d->dz_inv != nullptr;
+  // slab-interface sides need the neighbour element's metric terms in the face-wise y tables;
+  // on uniform grids the class tables hold both sides, per-face tables would be one-sided
+  for (int q = 0; q < 6; ++q)
+    if (!uniform && d->side_kind[q] >= HDGB_HALO_OWNED) {
+      delete c;
+      return einval("slab-interface sides need a uniform grid (per-face y tables would be one-sided)");
+    }
   {
     double h1 = d->widths[0][0], h2 = d->widths[1][0], h3 = d->widths[2][0];
     double a0 = h1 * h2 * h3 / 8.0, t1 = 2.0 / h1, t2 = 2.0 / h2, t3 = 2.0 / h3;

@@ -350,12 +350,14 @@ static cudaError_t launch_rhs_n(hdgb_ctx* c, const double* f, double* F, cudaStr
     if (c->uniform) {
       auto k = color ? rhs_kernel<N, 1, 1> : rhs_kernel<N, 0, 1>;
       if ((e = resident_grid(k, C::NT, smem, c->dev, cache[1][color], &grid)) != cudaSuccess) return e;
+      grid = cap_grid(c, grid);
       if (grid > npairs) grid = npairs;
       if (grid < 1) return cudaSuccess;
       k<<<(unsigned)grid, C::NT, smem, s>>>(a, f, npairs, K);
     } else {
       auto k = color ? rhs_kernel<N, 1, 0> : rhs_kernel<N, 0, 0>;
       if ((e = resident_grid(k, C::NT, smem, c->dev, cache[0][color], &grid)) != cudaSuccess) return e;
+      grid = cap_grid(c, grid);
       if (grid > npairs) grid = npairs;
       if (grid < 1) return cudaSuccess;
       k<<<(unsigned)grid, C::NT, smem, s>>>(a, f, npairs, K);
@@ -381,12 +383,14 @@ static cudaError_t launch_hyb_n(hdgb_ctx* c, const double* u0, const double* gN,
     if (c->uniform) {
       auto k = color ? hyb_kernel<N, 1, 1> : hyb_kernel<N, 0, 1>;
       if ((e = resident_grid(k, C::NT, smem, c->dev, cache[1][color], &grid)) != cudaSuccess) return e;
+      grid = cap_grid(c, grid);
       if (grid > npairs) grid = npairs;
       if (grid < 1) return cudaSuccess;
       k<<<(unsigned)grid, C::NT, smem, s>>>(a, u0, gN, npairs, K);
     } else {
       auto k = color ? hyb_kernel<N, 1, 0> : hyb_kernel<N, 0, 0>;
       if ((e = resident_grid(k, C::NT, smem, c->dev, cache[0][color], &grid)) != cudaSuccess) return e;
+      grid = cap_grid(c, grid);
       if (grid > npairs) grid = npairs;
       if (grid < 1) return cudaSuccess;
       k<<<(unsigned)grid, C::NT, smem, s>>>(a, u0, gN, npairs, K);
@@ -410,12 +414,14 @@ static cudaError_t launch_recover_n(hdgb_ctx* c, const double* f, const double* 
   if (c->uniform) {
     auto k = recover_kernel<N, 1>;
     if ((e = resident_grid(k, C::NT, smem, c->dev, cache[1], &grid)) != cudaSuccess) return e;
+    grid = cap_grid(c, grid);
     if (grid > c->g.ne) grid = c->g.ne;
     if (grid < 1) return cudaSuccess;
     k<<<(unsigned)grid, C::NT, smem, s>>>(a, f, tr, u, q, K);
   } else {
     auto k = recover_kernel<N, 0>;
     if ((e = resident_grid(k, C::NT, smem, c->dev, cache[0], &grid)) != cudaSuccess) return e;
+    grid = cap_grid(c, grid);
     if (grid > c->g.ne) grid = c->g.ne;
     if (grid < 1) return cudaSuccess;
     k<<<(unsigned)grid, C::NT, smem, s>>>(a, f, tr, u, q, K);

@@ -176,9 +176,10 @@ struct FxCfg {
 #define HDGB_FX_WIDE_N 13
 #endif
   // warps per CTA
-  // (the PCG variants at N = 17 stay narrow: block PCG p = 16 1396 -> 1196 us/iter)
+  // (the PCG variants at N = 17 stay narrow: block PCG p = 16 1396 -> 1196 us/iter; at N = 16 the
+  // three-operand pre-transform would need 233 KB of shared memory wide)
   static constexpr int WARPS =
-      (N >= HDGB_FX_WIDE_N && (FK == FX_TRANSFORM || FK == FX_POST) && !(CG && N >= 17)) ? 2 * HDGB_FX_WARPS
+      (N >= HDGB_FX_WIDE_N && (FK == FX_TRANSFORM || FK == FX_POST) && !(CG && N >= 16)) ? 2 * HDGB_FX_WARPS
                                                                                          : HDGB_FX_WARPS;
   static constexpr int NG = WARPS / GW;              // independent groups per CTA
   static constexpr int NT = 32 * WARPS;
@@ -925,7 +926,7 @@ static FaceArgs base_args(hdgb_ctx* c, int prec) {
 template <int N, int PREC, int FK, bool WITHZ, bool NOX = false>
 static cudaError_t pw_launch(hdgb_ctx* c, const FaceArgs& a, cudaStream_t s) {
   const int64_t n = c->n_all;
-  int grid = (int)min((int64_t)PW_GRID, (n + 256 * PW_U - 1) / (256 * PW_U));
+  int grid = (int)cap_grid(c, min((int64_t)PW_GRID, (n + 256 * PW_U - 1) / (256 * PW_U)));
   if (grid < 1) grid = 1;
   cudaError_t le = launch_pdl(pw_kernel<N, PREC, FK, WITHZ, NOX>, dim3(grid), dim3(256), 0, s, a, c->d_finfo, (unsigned)n);
   c->launches++;
@@ -982,6 +983,7 @@ static cudaError_t fx_launch(hdgb_ctx* c, const FaceArgs& a, const double* Ah, c
     else fold_n2e(Ah, N, c->sig, M.Af);
     if (nb_b == N * N) fold_e2n(Bh, N, c->sig, M.Bf);
   }
+  static_assert(sizeof(double) * C::smem_doubles() <= 227 * 1024, "face kernel shared memory exceeds 227 KB");
   const size_t smem = sizeof(double) * C::smem_doubles();
   auto k = fx_kernel<N, FK, CG>;
   static int cache[16] = {0};
@@ -990,6 +992,7 @@ static cudaError_t fx_launch(hdgb_ctx* c, const FaceArgs& a, const double* Ah, c
   if (e != cudaSuccess) return e;
   const int64_t nb = (c->nfaces + C::FPW * C::NG - 1) / (C::FPW * C::NG);
   if (grid > PW_GRID) grid = PW_GRID;
+  grid = cap_grid(c, grid);
   if (grid > nb) grid = nb;
   if (grid < 1) grid = 1;
   cudaError_t le = launch_pdl(k, dim3((unsigned)grid), dim3(C::NT), smem, s, a, c->d_finfo, c->d_fcoef, M);

@@ -314,7 +314,17 @@ struct hdgb_ctx {
   // HBM traffic (pass-0 partials stay in L2) but multiplies launches; while the element
   // kernels are issue-bound the single slab is faster (HDGB_SLAB_MB overrides).
   int64_t slab_bytes = 0;
+  // test knob (HDGB_GRID_CAP): upper bound on the persistent grids of the element and face
+  // kernels, so every CTA walks several element groups / face batches through its staging
+  // ring; 0 = the resident grid
+  int64_t grid_cap = 0;
 };
+
+namespace hdgb {
+inline int64_t cap_grid(const hdgb_ctx* c, int64_t grid) {
+  return (c->grid_cap > 0 && grid > c->grid_cap) ? c->grid_cap : grid;
+}
+}  // namespace hdgb
 
 namespace hdgb {
 void set_error(const std::string& msg);

@@ -263,25 +263,40 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   // TMA: warp 0 stages the group (lane 0 arms the barrier with the byte count, the lanes issue
   // one face copy each); the previous generic accesses of the buffer were fenced by the loop's
   // closing barrier, ordered before the async writes by fence.proxy.async
+  // Odd NQ: a face at an odd offset is copied with its 16-byte aligned cover [off - 1, off + NQ)
+  // (NQ + 1 doubles, data at slot + 1); a face at an even offset copies its first NQ - 1
+  // doubles and the lane loads the last one itself, so no copy reads past the face (the
+  // vector may end there).  The lanes' plain stores are ordered before the arrive by the
+  // warp barrier; the arrive's transaction count is the warp's sum of copied bytes (a
+  // complete_tx may land before the expect_tx: the count is allowed to go negative).
   auto stage_tma = [&](const ElemInfo* inf, double* buf, int bi) {
     if (tid >= 32) return;
-    constexpr uint32_t CNT = (NQ & 1) ? NQ + 1 : NQ;  // doubles per face copy (even)
     constexpr int NC = PUPD ? 18 : 6;
-    if (tid == 0) {
-      uint32_t nval = 0;
-      for (int ee = 0; ee < G; ++ee) nval += inf[ee].valid ? 1u : 0u;
-      fence_proxy_async();
-      mbar_expect_tx(&sBar[bi], nval * NC * CNT * 8u);
-    }
-    __syncwarp();
+    fence_proxy_async();  // the buffer's previous generic accesses (closing barrier) before the refill
+    uint32_t bytes = 0;
     for (int c = tid; c < G * NC; c += 32) {
       const int ee = c / NC, k = c - ee * NC, sface = k % 6;
       if (!inf[ee].valid) continue;
       const unsigned off = inf[ee].off[sface];
-      const unsigned lo = (NQ & 1) ? (off & ~1u) : off;
+      const double* src = k < 6 ? a.u : (k < 12 ? a.z : a.xout);
       double* dst = (k < 6 ? buf : (k < 12 ? sZ0 : sX0) + bi * G * FS) + ee * FS + sface * FSTR;
-      bulk_g2s(dst, (k < 6 ? a.u : (k < 12 ? a.z : a.xout)) + lo, CNT * 8u, &sBar[bi]);
+      uint32_t cnt = NQ;
+      unsigned lo = off;
+      if (NQ & 1) {
+        if (off & 1u) {
+          lo = off - 1u;
+          cnt = NQ + 1;
+        } else {
+          cnt = NQ - 1;
+          dst[NQ - 1] = src[off + NQ - 1];
+        }
+      }
+      bulk_g2s(dst, src + lo, cnt * 8u, &sBar[bi]);
+      bytes += cnt * 8u;
     }
+    bytes = __reduce_add_sync(0xffffffffu, bytes);
+    __syncwarp();
+    if (tid == 0) mbar_expect_tx(&sBar[bi], bytes);
   };
   auto stage = [&](const ElemInfo* inf, double* buf, int bi) {
     if (TMA) {
@@ -474,6 +489,8 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
 template <int N, int MODE, int COLOR>
 static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_t t1, cudaStream_t s) {
   using Cf = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>;
+  static_assert(sizeof(double) * Cf::smem_doubles((MODE & 9) == 9 && COLOR == 0) <= 227 * 1024,
+                "element kernel shared memory exceeds 227 KB");
   const size_t smem = sizeof(double) * (size_t)Cf::smem_doubles((MODE & 9) == 9 && COLOR == 0);
   auto kern = opV_kernel<N, MODE, COLOR>;
   static int cache[16] = {0};
@@ -481,6 +498,7 @@ static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
   cudaError_t e = resident_grid(kern, Cf::NT, smem, c->dev, cache, &grid);
   if (e != cudaSuccess) return e;
   const int64_t need = (t1 - t0 + Cf::G - 1) / Cf::G;
+  grid = cap_grid(c, grid);
   if (grid > need) grid = need;
   if (grid < 1) return cudaSuccess;
   TabOff to;

@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["slab_range", "slab_side_kinds", "slab_mesh", "SlabHalo", "slab_pcg", "SlabSystem"]
+__all__ = ["slab_range", "slab_side_kinds", "slab_mesh", "slab_local_index", "SlabHalo", "slab_pcg", "SlabSystem"]
 
 
 def slab_range(n1, rank, world):
@@ -50,6 +50,29 @@ def slab_mesh(global_n, lo, hi, rank, world, bc="dirichlet"):
     i0, i1 = slab_range(n1, rank, world)
     hx = (hi[0] - lo[0]) / n1
     return Mesh((i1 - i0, n2, n3), (lo[0] + i0 * hx, lo[1], lo[2]), (lo[0] + i1 * hx, hi[1], hi[2]), bc)
+
+
+def slab_local_index(global_n, n, rank, world):
+    """Global all-face index of every slot of the rank's local all-face vector.
+
+    Both layouts follow the reference face enumeration (mesh.py:113-126, 215-221); the
+    local grid is the slab [i0, i1) x n2 x n3, so local x-face plane l is global plane i0 + l
+    (interface planes appear on both neighbours).  `global_vec[idx]` scatters a global
+    vector to the rank, `global_vec[idx] = local_vec` gathers it back.
+    """
+    g1, g2, g3 = (int(v) for v in global_n)
+    i0, i1 = slab_range(g1, rank, world)
+    l1 = i1 - i0
+    n2f = n * n
+    goff = np.cumsum([0, (g1 + 1) * g2 * g3, g1 * (g2 + 1) * g3])
+    f = np.arange((l1 + 1) * g2 * g3)
+    x = goff[0] + (i0 + f % (l1 + 1)) + (g1 + 1) * (f // (l1 + 1))
+    f = np.arange(l1 * (g2 + 1) * g3)
+    y = goff[1] + (i0 + f % l1) + g1 * (f // l1)
+    f = np.arange(l1 * g2 * (g3 + 1))
+    z = goff[2] + (i0 + f % l1) + g1 * (f // l1)
+    faces = np.concatenate([x, y, z]).astype(np.int64)
+    return (faces[:, None] * n2f + np.arange(n2f)[None, :]).ravel()
 
 
 class SlabHalo:
