@@ -144,6 +144,11 @@ int hdgb_build_rhs(hdgb_ctx* ctx, const double* f, double* F, void* stream);
  * from f and the all-face trace. */
 int hdgb_recover_interior(hdgb_ctx* ctx, const double* f, const double* trace, double* u, double* q, void* stream);
 
+/* apply_element_inverse (solver.py:129-155): (u, q) = A^-1 (Fu, Fq) per element by fast
+ * diagonalisation.  Fu, u: n_e * n^3; Fq, q: 3 * n_e * n^3 (direction-major, element-major,
+ * a1 slowest).  Outputs must not alias the inputs. */
+int hdgb_element_inverse(hdgb_ctx* ctx, const double* Fu, const double* Fq, double* u, double* q, void* stream);
+
 /* Generic FP64 vector kernels for pcg() with arbitrary callables (solver.py:282-321). */
 int64_t hdgb_dot_scratch_doubles(void);
 /* *result_dev = sum_i x_i y_i (deterministic fixed-order reduction). */

@@ -68,6 +68,7 @@ SIGNATURES = {
     "hdgb_hybridize": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "hdgb_build_rhs": (ctypes.c_int, [_VP, _VP, _VP, _VP]),
     "hdgb_recover_interior": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
+    "hdgb_element_inverse": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
     "hdgb_face_dot": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
     "hdgb_vec_axpby": (ctypes.c_int, [_I64, _D, _VP, _D, _VP, _VP, _VP]),
     "hdgb_halo_pack": (ctypes.c_int, [_VP, _VP, ctypes.c_int, _VP, _VP]),

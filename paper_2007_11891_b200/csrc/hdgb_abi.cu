@@ -69,6 +69,7 @@ static void free_ctx(hdgb_ctx* c) {
   for (double* b : bufs)
     if (b) cudaFree(b);
   if (c->d_finfo) cudaFree(c->d_finfo);
+  if (c->d_wdone) cudaFree(c->d_wdone);
   if (c->d_st) cudaFree(c->d_st);
   if (c->h_st) cudaFreeHost(c->h_st);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
@@ -95,6 +96,7 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
   c->dev = d->device;
   if (const char* sb = getenv("HDGB_SLAB_MB")) c->slab_bytes = (int64_t)atof(sb) * (1LL << 20);
   if (const char* gc = getenv("HDGB_GRID_CAP")) c->grid_cap = atoll(gc);
+  if (const char* mg = getenv("HDGB_MERGE")) c->merge = atoi(mg);
   if (cudaSetDevice(c->dev) != cudaSuccess) {
     delete c;
     return einval("invalid CUDA device");
@@ -250,6 +252,11 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
     CK(cudaMemcpy(c->d_fcoef, fcoef.data(), sizeof(double) * c->nfaces, cudaMemcpyHostToDevice));
   }
   CK(cudaMalloc(&c->d_part, sizeof(double) * 4 * HDGB_RED_BLOCKS + 64));
+  {
+    const int64_t npairs = (int64_t)((g.n1 + 1) / 2) * g.n2 * g.n3;
+    CK(cudaMalloc(&c->d_wdone, sizeof(uint32_t) * (npairs + 2)));
+    CK(cudaMemset(c->d_wdone, 0, sizeof(uint32_t) * (npairs + 2)));
+  }
   CK(cudaMalloc(&c->d_st, sizeof(CGState)));
   CK(cudaMemset(c->d_st, 0, sizeof(CGState)));
   CK(cudaMallocHost(&c->h_st, sizeof(CGState)));
@@ -525,6 +532,15 @@ int hdgb_recover_interior(hdgb_ctx* c, const double* f, const double* trace, dou
   if (c->h_elem.empty()) return einval("element tables not set (hdgb_ctx_set_element_tables)");
   if (c->g.ne == 0) return HDGB_OK;
   HDGB_CUDA(launch_recover(c, f, trace, u, q, (cudaStream_t)stream));
+  return HDGB_OK;
+}
+
+int hdgb_element_inverse(hdgb_ctx* c, const double* Fu, const double* Fq, double* u, double* q, void* stream) {
+  if (!c || !Fu || !Fq || !u || !q) return einval("null argument");
+  if (c->h_elem.empty()) return einval("element tables not set (hdgb_ctx_set_element_tables)");
+  if (Fu == u || Fq == q) return einval("inputs and outputs must not alias");
+  if (c->g.ne == 0) return HDGB_OK;
+  HDGB_CUDA(launch_element_inverse(c, Fu, Fq, u, q, (cudaStream_t)stream));
   return HDGB_OK;
 }
 

@@ -27,6 +27,7 @@ struct ElemConst {
   double C[2 * N];   // C[a][s]
   double w[N];       // quadrature weights
   double Dh[N * N];  // Dhat = M^-1 D (nodal derivative)
+  double DM[N * N];  // D M^-1 (apply_element_inverse's q -> u coupling)
   double tau_hat;    // reference-element penalty
 };
 
@@ -227,6 +228,88 @@ __global__ void __launch_bounds__(ElemCfg<N>::NT) recover_kernel(const OpArgs a,
   }
 }
 
+// apply_element_inverse (solver.py:129-155) on arbitrary (Fu, Fq): w = Fu - sum_d (2/h_d) (D M^-1)_d Fq_d,
+// u = (S (x) S (x) S) dz_inv (S^T (x) S^T (x) S^T) w, q_d = -(2/h_d) (M^-1 D^T)_d u - M3^-1 Fq_d.
+// Fq and q are direction-major (3 x n_e x N^3).
+template <int N, int UNI>
+__global__ void __launch_bounds__(ElemCfg<N>::NT) inv_kernel(const OpArgs a, const double* __restrict__ Fu,
+                                                           const double* __restrict__ Fq, double* __restrict__ u,
+                                                           double* __restrict__ qout,
+                                                           const __grid_constant__ ElemConst<N> K) {
+  using C = ElemCfg<N>;
+  constexpr int NQ = C::NQ;
+  extern __shared__ __align__(16) double smem[];
+  double* vol = smem;
+  double* vq = smem + N * NQ;
+  __shared__ double sLam[N];
+  const int t = threadIdx.x;
+  const bool on = t < NQ;
+  const int t1 = t / N, t2 = t - (t / N) * N;
+  TabOff to;
+  to.set(N);
+  if (t < N) sLam[t] = a.tab[to.Lam + t];
+  const Geo& g = a.g;
+  const int64_t ne = g.ne, nv = (int64_t)N * NQ;
+  for (int64_t e = blockIdx.x; e < ne; e += gridDim.x) {
+    int c[3];
+    c[0] = (int)(e % g.n1);
+    c[1] = (int)((e / g.n1) % g.n2);
+    c[2] = (int)(e / ((int64_t)g.n1 * g.n2));
+    double al[4];
+    elem_alpha(a, c, al);
+    const double h[3] = {a.widths[c[0]], a.widths[g.n1 + c[1]], a.widths[g.n1 + g.n2 + c[2]]};
+    __syncthreads();
+    for (int q = t; q < N * NQ; q += blockDim.x) vol[q] = Fu[e * nv + q];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      __syncthreads();
+      for (int q = t; q < N * NQ; q += blockDim.x) vq[q] = Fq[(d * ne + e) * nv + q];
+      __syncthreads();
+      if (on) {  // w -= (2/h_d) (D M^-1) Fq_d along axis d, on the thread's own line
+        double x[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+          x[k] = vq[d == 0 ? vidx<N, 0>(k, t1, t2) : (d == 1 ? vidx<N, 1>(k, t1, t2) : vidx<N, 2>(k, t1, t2))];
+        const double th = 2.0 / h[d];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double s = K.DM[i * N] * x[0];
+#pragma unroll
+          for (int k = 1; k < N; ++k) s = fma(K.DM[i * N + k], x[k], s);
+          const int q = d == 0 ? vidx<N, 0>(i, t1, t2) : (d == 1 ? vidx<N, 1>(i, t1, t2) : vidx<N, 2>(i, t1, t2));
+          vol[q] -= th * s;
+        }
+      }
+    }
+    __syncthreads();
+    fast_diag<N, UNI>(K, vol, a.dz, sLam, al, a.lam * al[0], t, on);
+    for (int q = t; q < N * NQ; q += blockDim.x) u[e * nv + q] = vol[q];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      if (on) {
+        double x[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+          x[k] = vol[d == 0 ? vidx<N, 0>(k, t1, t2) : (d == 1 ? vidx<N, 1>(k, t1, t2) : vidx<N, 2>(k, t1, t2))];
+        const double tq = -2.0 / h[d];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double s = K.MD[i * N] * x[0];
+#pragma unroll
+          for (int k = 1; k < N; ++k) s = fma(K.MD[i * N + k], x[k], s);
+          const int q = d == 0 ? vidx<N, 0>(i, t1, t2) : (d == 1 ? vidx<N, 1>(i, t1, t2) : vidx<N, 2>(i, t1, t2));
+          const int i1 = q / NQ, i2 = (q / N) % N, i3 = q % N;
+          const double m3 = al[0] * (K.w[i1] * K.w[i2] * K.w[i3]);
+          vq[q] = tq * s - Fq[(d * ne + e) * nv + q] / m3;
+        }
+      }
+      __syncthreads();
+      for (int q = t; q < N * NQ; q += blockDim.x) qout[(d * ne + e) * nv + q] = vq[q];
+      __syncthreads();
+    }
+  }
+}
+
 template <int N>
 static ElemConst<N> elem_const(const hdgb_ctx* c) {
   ElemConst<N> K;
@@ -240,7 +323,10 @@ static ElemConst<N> elem_const(const hdgb_ctx* c) {
   const double* Cm = B + 2 * N;
   K.tau_hat = Cm[2 * N];
   for (int i = 0; i < N; ++i)
-    for (int k = 0; k < N; ++k) K.Dh[i * N + k] = D[i * N + k] / K.w[i];
+    for (int k = 0; k < N; ++k) {
+      K.Dh[i * N + k] = D[i * N + k] / K.w[i];
+      K.DM[i * N + k] = D[i * N + k] / K.w[k];
+    }
   // MD = M^-1 D^T : MD[i][k] = D[k][i] / w[i]
   for (int i = 0; i < N; ++i)
     for (int k = 0; k < N; ++k) K.MD[i * N + k] = D[k * N + i] / K.w[i];
@@ -428,6 +514,40 @@ static cudaError_t launch_recover_n(hdgb_ctx* c, const double* f, const double* 
   }
   c->launches++;
   return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t launch_inv_n(hdgb_ctx* c, const double* Fu, const double* Fq, double* u, double* q,
+                                cudaStream_t s) {
+  using C = ElemCfg<N>;
+  const ElemConst<N> K = elem_const<N>(c);
+  OpArgs a = elem_args(c);
+  const size_t smem = sizeof(double) * 2 * N * C::NQ;
+  static int cache[2][16] = {};
+  int64_t grid = 0;
+  cudaError_t e;
+  auto k = c->uniform ? inv_kernel<N, 1> : inv_kernel<N, 0>;
+  if ((e = resident_grid(k, C::NT, smem, c->dev, cache[c->uniform ? 1 : 0], &grid)) != cudaSuccess) return e;
+  grid = cap_grid(c, grid);
+  if (grid > c->g.ne) grid = c->g.ne;
+  if (grid < 1) return cudaSuccess;
+  k<<<(unsigned)grid, C::NT, smem, s>>>(a, Fu, Fq, u, q, K);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_element_inverse(hdgb_ctx* c, const double* Fu, const double* Fq, double* u, double* q,
+                                   cudaStream_t s) {
+  switch (c->N) {
+#define HDGB_CASE(n) \
+  case n:            \
+    return launch_inv_n<n>(c, Fu, Fq, u, q, s);
+    HDGB_CASE(2) HDGB_CASE(3) HDGB_CASE(4) HDGB_CASE(5) HDGB_CASE(6) HDGB_CASE(7) HDGB_CASE(8) HDGB_CASE(9)
+    HDGB_CASE(10) HDGB_CASE(11) HDGB_CASE(12) HDGB_CASE(13) HDGB_CASE(14) HDGB_CASE(15) HDGB_CASE(16)
+    HDGB_CASE(17)
+#undef HDGB_CASE
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_build_rhs(hdgb_ctx* c, const double* f, double* F, cudaStream_t s) {

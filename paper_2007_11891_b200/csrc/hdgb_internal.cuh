@@ -125,6 +125,9 @@ struct OpArgs {
   const double* z;       // CG mode, fused direction update: z (u = p is updated in place via pout)
   double* pout;
   double* xout;          // CG mode, fused direction update: x (deferred x += alpha_prev p_prev)
+  uint32_t* wdone;       // merged colour schedule: per-wave colour-0 arrivals (+ exit ticket)
+  int64_t wcount;        //   waves per colour
+  int64_t wlag;          //   colour-0 waves ahead of colour-1 wave 0
 };
 
 struct FaceArgs {
@@ -318,6 +321,11 @@ struct hdgb_ctx {
   // kernels, so every CTA walks several element groups / face batches through its staging
   // ring; 0 = the resident grid
   int64_t grid_cap = 0;
+  // merged colour schedule of the element kernel (both passes in one launch, L2-ordered):
+  // per-wave arrival counters (npairs + 2 words, zero between launches); HDGB_MERGE=0 runs the
+  // two colour passes as separate launches
+  uint32_t* d_wdone = nullptr;
+  int merge = 1;
 };
 
 namespace hdgb {
@@ -340,6 +348,8 @@ cudaError_t launch_face_transform_pupd(hdgb_ctx* c, const double* A_host, const 
 cudaError_t launch_build_rhs(hdgb_ctx* c, const double* f, double* F, cudaStream_t s);
 cudaError_t launch_hybridize(hdgb_ctx* c, const double* u0, const double* gN, double* x, cudaStream_t s);
 cudaError_t launch_recover(hdgb_ctx* c, const double* f, const double* tr, double* u, double* q, cudaStream_t s);
+cudaError_t launch_element_inverse(hdgb_ctx* c, const double* Fu, const double* Fq, double* u, double* q,
+                                   cudaStream_t s);
 cudaError_t launch_prec(hdgb_ctx* c, int kind, const double* in, double* out, cudaStream_t s);
 cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s, cudaGraphConditionalHandle loop = 0,
                              int loop_on = 0);

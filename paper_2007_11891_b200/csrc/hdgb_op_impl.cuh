@@ -177,6 +177,42 @@ struct ElemInfo {
   int kind[6];
 };
 
+// Merged colour schedule (COLOR = 2): both colour passes in one persistent launch.  Each CTA
+// walks 2 W slots (W = waves of element groups per colour, one group per CTA per wave) in the
+// order c0 waves 0..L-1, then c1 wave 0, c0 wave L, c1 wave 1, c0 wave L+1, ..., and the last
+// L c1 waves.  A colour-1 group of wave w needs the colour-0 groups of its x/y/z neighbours,
+// all in c0 waves <= w + L - 1 (L = 2 + (pairs per z-layer - 1) / (pairs per wave)), which
+// every CTA has finished before it reaches that slot; a per-wave counter (one arrival per CTA)
+// confirms it.  The colour-0 partials are therefore still L2-resident when colour 1 adds to
+// them, and u read by colour 1 was read by colour 0 one z-layer earlier: the DRAM traffic of
+// the pair approaches read u once + write r once.
+__device__ __forceinline__ void merged_slot(int64_t k, int64_t W, int64_t L, int& col, int64_t& w) {
+  if (W <= L) {
+    col = k < W ? 0 : 1;
+    w = k < W ? k : k - W;
+    return;
+  }
+  if (k < L) {
+    col = 0;
+    w = k;
+    return;
+  }
+  const int64_t m = k - L;
+  if (m < 2 * (W - L)) {
+    col = (m & 1) ? 0 : 1;
+    w = (m & 1) ? L + (m >> 1) : (m >> 1);
+    return;
+  }
+  col = 1;
+  w = (W - L) + (m - 2 * (W - L));
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // MODE bit 0: CG (Dirichlet rows -> 0, <p, w> and alpha from a fixed-order reduction at the end); bit 1: non-uniform grid (per-element
 // metric terms and dz_inv); bit 2: "g only" (plain core: emit the eigen-space sum of g only).
 template <int N, int MODE, int COLOR>
@@ -232,12 +268,28 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   }
 
   const int64_t ngroups = (t1 - t0 + G - 1) / G;
-  auto info = [&](int64_t gi, ElemInfo* dst) {
+  // slot k of this CTA -> (colour, element group)
+  const int64_t nslots = COLOR == 2 ? 2 * (int64_t)a.wcount
+                                    : ((int64_t)blockIdx.x < ngroups ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0);
+  auto slot_item = [&](int64_t k, int& col, int64_t& gi, int64_t& w) {
+    if (COLOR == 2) {
+      merged_slot(k, a.wcount, a.wlag, col, w);
+      gi = w * gridDim.x + blockIdx.x;
+    } else {
+      col = COLOR;
+      w = k;
+      gi = blockIdx.x + k * (int64_t)gridDim.x;
+    }
+  };
+  auto info = [&](int64_t k, ElemInfo* dst) {
     if (tid < G) {
       ElemInfo& I = dst[tid];
+      int col;
+      int64_t gi, w;
+      slot_item(k, col, gi, w);
       const int64_t t = t0 + gi * G + tid;
       Elem E;
-      I.valid = t < t1 && pair_elem(g, t, COLOR, E);
+      I.valid = gi < ngroups && t < t1 && pair_elem(g, t, col, E);
       if (I.valid) {
         double al[4];
         elem_alpha(a, E.c, al);
@@ -319,20 +371,30 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   };
 
   double dacc = 0.0;  // CG: this thread's share of <p, w> (fixed grid -> reproducible)
-  int64_t gi = blockIdx.x;
-  if (gi < ngroups) info(gi, sInfo[0]);
+  int64_t verified = -1;  // merged schedule: colour-0 waves known complete (thread 0)
+  if (nslots > 0) info(0, sInfo[0]);
   __syncthreads();
   if (!CG) pdl_wait();  // u and r come from earlier kernels
-  if (gi < ngroups) stage(sInfo[0], sF0, 0);
+  if (nslots > 0) stage(sInfo[0], sF0, 0);
   cp_async_commit();
-  for (int buf = 0, k = 0; gi < ngroups; gi += gridDim.x, buf ^= 1, ++k) {
-    const int64_t gn = gi + gridDim.x;
-    if (gn < ngroups) info(gn, sInfo[buf ^ 1]);
+  for (int64_t k = 0; k < nslots; ++k) {
+    const int buf = (int)(k & 1);
+    if (k + 1 < nslots) info(k + 1, sInfo[buf ^ 1]);
     __syncthreads();
-    if (gn < ngroups) stage(sInfo[buf ^ 1], sF0 + (buf ^ 1) * G * FS, buf ^ 1);
+    if (k + 1 < nslots) stage(sInfo[buf ^ 1], sF0 + (buf ^ 1) * G * FS, buf ^ 1);
     cp_async_commit();
     if (TMA) mbar_wait(&sBar[buf], (uint32_t)(k >> 1) & 1u);
     else asm volatile("cp.async.wait_group 1;\n" ::);
+    int col;
+    int64_t gi_unused, wave;
+    slot_item(k, col, gi_unused, wave);
+    if (COLOR == 2 && col == 1 && tid == 0) {  // the colour-0 neighbours of this wave are complete
+      const int64_t need = min((int64_t)a.wcount - 1, wave + (int64_t)a.wlag - 1);
+      for (int64_t v = verified + 1; v <= need; ++v)
+        while (ld_acquire_u32(a.wdone + v) < gridDim.x) {
+        }
+      verified = need > verified ? need : verified;
+    }
     // element geometry into registers once (sInfo[buf] was published a barrier ago)
     const ElemInfo& I = sInfo[buf][act ? e : 0];
     const bool on = act && I.valid;
@@ -367,7 +429,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     __syncthreads();  // staged faces (and their update) visible to the whole CTA
     // colour-0 partials of the shared faces at q: issued now, consumed at the emits
     double prev[6];
-    if (COLOR == 1 && on) {
+    if (col == 1 && on) {
 #pragma unroll
       for (int s = 0; s < 6; ++s) prev[s] = (shared >> s & 1u) ? __ldcg(a.r + off[s]) : 0.0;
     }
@@ -376,8 +438,8 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     auto emit = [&](int s, double gval, double ua, double ur) {
       const bool sh = shared >> s & 1u;
       double val = GONLY ? gval : ((s & 1) ? gcc1 : gcc0) * ua - gval;
-      if (COLOR == 1 && sh) val = prev[s] + val;
-      if (CG && (COLOR == 1 || !sh)) {  // final value of w here: Dirichlet row -> 0, <p, w>
+      if (col == 1 && sh) val = prev[s] + val;
+      if (CG && (col == 1 || !sh)) {  // final value of w here: Dirichlet row -> 0, <p, w>
         if (kinds[s] == HDGB_DIRICHLET) val = 0.0;
         if (kind_counts(kinds[s])) dacc = fma(ur, val, dacc);
       }
@@ -429,8 +491,22 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       emit(5, al3 * az1, al3 * zr1, zr1);
     }
     __syncthreads();  // staging buffer, volume and element info are reused
+    if (COLOR == 2 && col == 0 && tid == 0) {  // this CTA's colour-0 group of the wave is stored
+      __threadfence();
+      atomicAdd(a.wdone + wave, 1u);
+    }
   }
   cp_async_wait_all();
+  if (COLOR == 2) {  // the last CTA out resets the wave counters for the next launch
+    if (tid == 0) {
+      __threadfence();
+      const uint32_t t = atomicAdd(a.wdone + a.wcount, 1u);
+      if (t == gridDim.x - 1) {
+        for (int64_t v = 0; v <= a.wcount; ++v) a.wdone[v] = 0u;
+        __threadfence();
+      }
+    }
+  }
   if (PUPD) {  // boundary faces of colour-1 elements (no colour-0 neighbour): one warp per face
     const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
     const int64_t nb0 = 2LL * g.n2 * g.n3, nb1 = 2LL * g.n1 * g.n3, nb = nb0 + nb1 + 2LL * g.n1 * g.n2;
@@ -480,7 +556,8 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       final_sum2(a.part, gridDim.x, tot, t2);
       if (threadIdx.x == 0) {
         if (COLOR == 0) a.st->pw0 = tot;
-        else cg_set_alpha(a.st, a.st->pw0 + tot);
+        else if (COLOR == 1) cg_set_alpha(a.st, a.st->pw0 + tot);
+        else cg_set_alpha(a.st, tot);
       }
     }
   }
@@ -501,6 +578,14 @@ static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
   grid = cap_grid(c, grid);
   if (grid > need) grid = need;
   if (grid < 1) return cudaSuccess;
+  OpArgs am = a;
+  if (COLOR == 2) {  // merged schedule: waves per colour and the colour-0 lead (see merged_slot)
+    const int64_t per_k = (int64_t)((c->g.n1 + 1) / 2) * c->g.n2;  // element pairs per z-layer
+    const int64_t per_wave = grid * Cf::G;
+    am.wdone = c->d_wdone;
+    am.wcount = (need + grid - 1) / grid;
+    am.wlag = 2 + (per_k > 0 ? (per_k - 1) / per_wave : 0);
+  }
   TabOff to;
   to.set(N);
   OpVConst<N> K;
@@ -509,7 +594,7 @@ static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
     K.B1[q] = c->h_tab[to.BS + 2 * q + 1];
     K.Lam[q] = c->h_tab[to.Lam + q];
   }
-  cudaError_t le = launch_pdl(kern, dim3((unsigned)grid), dim3(Cf::NT), smem, s, a, t0, t1, K);
+  cudaError_t le = launch_pdl(kern, dim3((unsigned)grid), dim3(Cf::NT), smem, s, am, t0, t1, K);
   c->launches++;
   return le;
 }
@@ -570,6 +655,13 @@ static cudaError_t launch_t(hdgb_ctx* c, const double* u, double* r, cudaStream_
       return c->uniform ? launch_any<N, false, MODE, 1>(c, a, 0, t1, s)
                         : launch_any<N, false, MODE | 2, 1>(c, a, 0, t1, s);
     }
+  }
+  if (c->merge && nslab == 1) {  // both colour passes in one L2-ordered launch
+    const int64_t t1 = g.n3 * per_k;
+    e = c->uniform ? launch_any<N, PLAIN, MODE, 2>(c, a, 0, t1, s) : launch_any<N, PLAIN, MODE | 2, 2>(c, a, 0, t1, s);
+    if (e != cudaSuccess) return e;
+    if (PLAIN) return launch_plain_post(c, MODE & 1, u, r, s);
+    return cudaSuccess;
   }
   for (int64_t sl = 0; sl <= nslab; ++sl) {
     if (sl < nslab) {

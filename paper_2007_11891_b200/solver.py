@@ -10,13 +10,12 @@ the library's deterministic FP64 dot/axpby kernels.
 
 Pre/post steps (element inverse by fast diagonalisation, RHS with
 Dirichlet lift, hybridised initial guess, interior recovery;
-solver.py:129-279; SURVEY §8f "next" #1): `solve` / `solve_transformed`
-run the element RHS and the interior recovery on the device
-(csrc/hdgb_elem.cu) and keep every vector device-resident from the RHS to
-(u, q), with the reference's FlopCounter totals added analytically; the host
-restatements below (generalised to per-element geometry for non-uniform
-grids) remain the public pre/post functions and the parity reference of the
-device versions (`solve_host_pipeline`).
+solver.py:129-279; SURVEY §8f "next" #1) run on the device
+(csrc/hdgb_elem.cu): the public functions keep the reference signatures and
+return new host arrays, and `solve` / `solve_transformed` keep every vector
+device-resident from the RHS to (u, q), with the reference's FlopCounter
+totals added analytically.  Their host restatement, the parity checker, is
+test infrastructure (oracle/host_prepost.py).
 """
 
 import math
@@ -27,21 +26,13 @@ import numpy as np
 
 from . import _lib
 from .basis import Basis1D
-from .mesh import (DIRICHLET, NEUMANN, FluxField, gather_batched, pack_all, pack_unknowns, scatter_add_batched,
-                   unpack_unknowns)
-from .operator import OperatorContext, device_context, hdg_op_3d, transform_faces
-from .preconditioner import (
-    BlockPreconditioner,
-    DiagonalPreconditioner,
-    _DevicePrecBase,
-    build_block_preconditioner,
-    build_diagonal_preconditioner,
-    transformed_preconditioner,
-)
+from .mesh import DIRICHLET, NEUMANN, DeviceFluxField, FluxField, pack_all
+from .operator import OperatorContext, device_context
+from .preconditioner import _DevicePrecBase, build_block_preconditioner, build_diagonal_preconditioner
 
 __all__ = ["SolverConfig", "SolveReport", "make_context", "resolve_tau_hat", "apply_element_inverse",
            "hybridize_initial_guess", "build_rhs", "recover_interior", "pcg", "solve", "solve_transformed",
-           "solve_host_pipeline", "solve_transformed_host_pipeline", "solve_flop_count", "DeviceOperator"]
+           "solve_flop_count", "DeviceOperator"]
 
 PRECONDITIONER_KINDS = ("none", "diagonal", "block", "transformed")
 
@@ -139,7 +130,7 @@ def _fused_plan(apply_K, apply_P):
     return None
 
 
-def _pcg_fused(plan, F, x0, rtol, atol, max_iters):
+def _pcg_fused(plan, F, x0, rtol, atol, max_iters, ctx=None):
     import torch
 
     dc, variant, kind = plan
@@ -154,6 +145,9 @@ def _pcg_fused(plan, F, x0, rtol, atol, max_iters):
     Fa = dc.unpack(up(F))
     xa = dc.unpack(up(x0))
     it, rel, conv = dc.pcg(variant, kind, Fa, xa, rtol, atol, max_iters)
+    if ctx is not None and getattr(ctx, "counter", None) is not None:  # the K applies apply_K would count
+        n = dc.n
+        ctx.counter.ops += (it + 1) * ctx.mesh.n_elements * ((73 if variant == _lib.PLAIN else 25) * n ** 3 + 12 * n ** 2)
     x = dc.pack(xa)
     if as_np:
         x = dc.download([x])[0]
@@ -257,156 +251,20 @@ def pcg(apply_K, apply_P, F, x0, rtol=1e-10, atol=0.0, max_iters=10000):
     """
     plan = _fused_plan(apply_K, apply_P)
     if plan is not None:
-        return _pcg_fused(plan, F, x0, rtol, atol, max_iters)
+        return _pcg_fused(plan, F, x0, rtol, atol, max_iters, apply_K.ctx)
     return _pcg_generic(apply_K, apply_P, F, x0, rtol, atol, max_iters)
 
 
-# ============================================================================ host pre/post
-class _ElemGeom:
-    """Per-element metric factors as broadcastable arrays (scalars on uniform grids)."""
-
-    def __init__(self, ctx):
-        mesh = ctx.mesh
-        b = ctx.basis
-        w = b.weights
-        self.uniform = getattr(mesh, "uniform", True)
-        wprod = w[:, None, None] * w[None, :, None] * w[None, None, :]
-        if self.uniform:
-            g = ctx.geom
-            self.two_over_h = [np.float64(t) for t in ctx.two_over_h]
-            self.alphas = [np.float64(a) for a in g.alphas]
-            self.half = [np.float64(hw) for hw in g.half_widths]
-            self.dz = ctx.dz_inv[None]
-            self.mass3 = ctx.mass3[None]
-            self.inv_mass3 = ctx.inv_mass3[None]
-        else:
-            h = mesh.element_widths()
-            a0 = h.prod(axis=1) / 8.0
-            al = a0[:, None] * (2.0 / h) ** 2
-            col = lambda v: v[:, None, None, None]  # noqa: E731
-            self.two_over_h = [col(2.0 / h[:, d]) for d in range(3)]
-            self.alphas = [col(al[:, d]) for d in range(3)]
-            self.half = [col(0.5 * h[:, d]) for d in range(3)]
-            L = b.Lambda
-            den = (ctx.lam * a0[:, None, None, None] + al[:, 0, None, None, None] * L[None, :, None, None]
-                   + al[:, 1, None, None, None] * L[None, None, :, None]
-                   + al[:, 2, None, None, None] * L[None, None, None, :])
-            self.dz = 1.0 / den
-            self.mass3 = col(a0) * wprod[None]
-            self.inv_mass3 = 1.0 / self.mass3
-
-
-def _geom(ctx):
-    g = getattr(ctx, "_hdgb_elem_geom", None)
-    if g is None:
-        g = _ElemGeom(ctx)
-        try:
-            ctx._hdgb_elem_geom = g
-        except AttributeError:
-            pass
-    return g
-
-
-def _axis(A, x, axis):
-    """Contract matrix A (m, k) with tensor x along `axis`."""
-    return np.moveaxis(np.moveaxis(x, axis, -1) @ A.T, -1, axis)
-
-
-def _face_tang_w(ctx, d):
-    w = ctx.basis.weights
-    n = ctx.basis.n
-    t1, t2 = [t for t in range(3) if t != d]
-    w2 = np.multiply.outer(w, w)
-    return w2.reshape([n if i in (1 + t1, 1 + t2) else 1 for i in range(4)])
-
-
-def apply_element_inverse(Fu, Fq, ctx):
-    """Interior block inverse by fast diagonalisation (solver.py:129-155), per-element geometry."""
-    g = _geom(ctx)
-    b = ctx.basis
-    S = b.S
-    DMinv = b.D * b.inv_weights[None, :]
-    MinvDT = b.inv_weights[:, None] * b.D.T
-    w = np.array(Fu, dtype=float, copy=True)
-    for d in range(3):
-        w -= g.two_over_h[d] * _axis(DMinv, Fq[d], 1 + d)
-    for d in range(3):
-        w = _axis(S.T, w, 1 + d)
-    w *= g.dz
-    for d in range(3):
-        w = _axis(S, w, 1 + d)
-    qs = tuple(-g.two_over_h[d] * _axis(MinvDT, w, 1 + d) - g.inv_mass3 * Fq[d] for d in range(3))
-    return w, qs
-
-
-def _face_tau(ctx, d):
-    """Per-face penalty (2/h_d) tau_hat; on non-uniform grids the mean of the two sides."""
-    mesh = ctx.mesh
-    tau_hat = ctx.basis.tau_hat
-    if getattr(mesh, "uniform", True):
-        return (2.0 / mesh.h[d]) * tau_hat
-    nf = mesh.n_faces[d]
-    acc, cnt = np.zeros(nf), np.zeros(nf)
-    hd = mesh.element_widths()[:, d]
-    for faces in (mesh.face_lo[d], mesh.face_hi[d]):
-        np.add.at(acc, faces, 2.0 / hd * tau_hat)
-        np.add.at(cnt, faces, 1.0)
-    return (acc / cnt)[:, None, None]
-
-
-def hybridize_initial_guess(u, ctx, g_D=None, g_N=None):
-    """Trace consistent with an interior field u (solver.py:158-195)."""
-    mesh = ctx.mesh
-    n = ctx.basis.n
-    g = _geom(ctx)
-    u = np.asarray(u, dtype=float).reshape(mesh.n_elements, n, n, n)
-    field = FluxField(mesh, ctx.basis.p)
-    for d in range(3):
-        q = g.two_over_h[d] * _axis(ctx.basis.Dhat, u, 1 + d)
-        nf = mesh.n_faces[d]
-        usum = np.zeros((nf, n, n))
-        qnsum = np.zeros((nf, n, n))
-        usum[mesh.face_lo[d]] += np.take(u, 0, axis=1 + d)
-        usum[mesh.face_hi[d]] += np.take(u, n - 1, axis=1 + d)
-        qnsum[mesh.face_lo[d]] += -np.take(q, 0, axis=1 + d)
-        qnsum[mesh.face_hi[d]] += np.take(q, n - 1, axis=1 + d)
-        tau = _face_tau(ctx, d)
-        kind = mesh.face_kind[d]
-        vals = 0.5 * usum - qnsum / (2.0 * tau)
-        neu = kind == NEUMANN
-        if np.any(neu):
-            gn = g_N.data[d][neu] if g_N is not None else 0.0
-            tn = tau if np.ndim(tau) == 0 else tau[neu]
-            vals[neu] = usum[neu] - (qnsum[neu] - gn) / tn
-        dir_ = kind == DIRICHLET
-        vals[dir_] = g_D.data[d][dir_] if g_D is not None else 0.0
-        field.data[d] = vals
-    return field
-
-
-def _flux_couplings(ctx, u, qs):
-    g = _geom(ctx)
-    b = ctx.basis
-    out = []
-    for d in range(3):
-        tw = _face_tang_w(ctx, d)
-        y = _axis(b.B.T, u, 1 + d) * (g.alphas[d] * tw)
-        z = _axis(b.C.T, qs[d], 1 + d) * (g.half[d] * g.alphas[d] * tw)
-        out.append(y + z)
-    return out
-
-
+# ============================================================================ pre/post (device)
 def _face_mass(ctx, d):
+    """Neumann face mass (h_t1/2)(h_t2/2) (w (x) w) per face (solver.py:233-237, ctx.face_mass)."""
     mesh = ctx.mesh
     w = ctx.basis.weights
     w2 = np.multiply.outer(w, w)
     t1, t2 = [t for t in range(3) if t != d]
     if getattr(mesh, "uniform", True):
         return (0.5 * mesh.h[t1]) * (0.5 * mesh.h[t2]) * w2[None]
-    coords = mesh.face_node_grids(d, ctx.basis.nodes)  # only for shape bookkeeping
-    del coords
-    nf = mesh.n_faces[d]
-    f = np.arange(nf)
+    f = np.arange(mesh.n_faces[d])
     n1, n2, _ = mesh.n
     if d == 0:
         i1, i2 = (f // (n1 + 1)) % n2, f // ((n1 + 1) * n2)
@@ -418,54 +276,6 @@ def _face_mass(ctx, d):
     return hw[:, None, None] * w2[None]
 
 
-def build_rhs(f, g_D, g_N, ctx):
-    """Condensed right-hand side with Neumann data and Dirichlet lift (solver.py:212-251)."""
-    mesh = ctx.mesh
-    n = ctx.basis.n
-    g = _geom(ctx)
-    f = np.asarray(f, dtype=float).reshape(mesh.n_elements, n, n, n)
-    Fu = g.mass3 * f
-    zeros = tuple(np.zeros_like(Fu) for _ in range(3))
-    u, qs = apply_element_inverse(Fu, zeros, ctx)
-    F = FluxField(mesh, ctx.basis.p)
-    scatter_add_batched([-blk for blk in _flux_couplings(ctx, u, qs)], F, include_dirichlet=True)
-    if g_N is not None:
-        for d in range(3):
-            m = mesh.face_kind[d] == NEUMANN
-            if np.any(m):
-                fm = _face_mass(ctx, d)
-                F.data[d][m] += (fm[0] if fm.shape[0] == 1 else fm[m]) * g_N.data[d][m]
-    if g_D is not None:
-        lift = FluxField(mesh, ctx.basis.p)
-        nonzero = False
-        for d in range(3):
-            m = mesh.face_kind[d] == DIRICHLET
-            lift.data[d][m] = g_D.data[d][m]
-            nonzero = nonzero or bool(np.any(lift.data[d]))
-        if nonzero:
-            Klift = hdg_op_3d(lift, ctx)  # device operator
-            for d in range(3):
-                F.data[d] -= Klift.data[d]
-    return F.zero_dirichlet()
-
-
-def recover_interior(f, u_tilde, ctx):
-    """Interior solution and gradient from the trace (solver.py:254-279)."""
-    mesh = ctx.mesh
-    n = ctx.basis.n
-    g = _geom(ctx)
-    b = ctx.basis
-    f = np.asarray(f, dtype=float).reshape(mesh.n_elements, n, n, n)
-    blocks = gather_batched(u_tilde)
-    Fu = g.mass3 * f
-    Fq = []
-    for d in range(3):
-        tw = _face_tang_w(ctx, d)
-        Fu = Fu - _axis(b.B, blocks[d] * (g.alphas[d] * tw), 1 + d)
-        Fq.append(-_axis(b.C, blocks[d] * (g.half[d] * g.alphas[d] * tw), 1 + d))
-    return apply_element_inverse(Fu, tuple(Fq), ctx)
-
-
 def _restore_dirichlet(flux, g_D):
     if g_D is None:
         flux.zero_dirichlet()
@@ -474,6 +284,148 @@ def _restore_dirichlet(flux, g_D):
     for d in range(3):
         m = mesh.face_kind[d] == DIRICHLET
         flux.data[d][m] = g_D.data[d][m]
+
+
+def _upload(dc, a):
+    import torch
+
+    if isinstance(a, torch.Tensor):
+        return a.to(f"cuda:{dc.device}", torch.float64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(f"cuda:{dc.device}")
+
+
+def _all_faces(field):
+    """All-face vector (pack_all order) of a FluxField, DeviceFluxField or flat array."""
+    if isinstance(field, DeviceFluxField):
+        return field.flat
+    if isinstance(field, FluxField):
+        return pack_all(field)
+    return field
+
+
+def _field(mesh, p, allv):
+    n = p + 1
+    out, off = [], 0
+    for d in range(3):
+        cnt = mesh.n_faces[d] * n * n
+        out.append(allv[off:off + cnt].reshape(mesh.n_faces[d], n, n))
+        off += cnt
+    return FluxField(mesh, p, out)
+
+
+def _kind_faces(ctx, field, kind, scale=None):
+    """All-face numpy vector holding `field` (times `scale`) on the faces of `kind`, else 0; None if empty."""
+    if field is None:
+        return None
+    mesh, p = ctx.mesh, ctx.basis.p
+    out = FluxField(mesh, p)
+    any_ = False
+    for d in range(3):
+        m = mesh.face_kind[d] == kind
+        if np.any(m):
+            v = field.data[d][m]
+            if scale is not None:
+                fm = scale(ctx, d)
+                v = (fm[0] if fm.shape[0] == 1 else fm[m]) * v
+            out.data[d][m] = v
+            any_ = any_ or bool(np.any(v))
+    return pack_all(out) if any_ else None
+
+
+def _count(ctx, ops):
+    c = getattr(ctx, "counter", None)
+    if c is not None:
+        c.ops += int(ops)
+
+
+def _inverse_ops(ctx):
+    n = ctx.basis.n
+    V = ctx.mesh.n_elements * n ** 3
+    return 24 * n * V + V
+
+
+def _device_rhs(ctx, dc, fd, g_D, g_N):
+    """build_rhs (solver.py:212-251) on the device: element part (hdgb_build_rhs), Neumann face
+    integral, Dirichlet lift F -= K g_D (the device plain operator), Dirichlet rows zeroed.
+    Returns (F, lift) as device all-face vectors (lift None when g_D is zero)."""
+    F = dc.build_rhs(fd)
+    neu = _kind_faces(ctx, g_N, NEUMANN, _face_mass)
+    if neu is not None:
+        F += _upload(dc, neu)
+    lift = _kind_faces(ctx, g_D, DIRICHLET)
+    if lift is not None:
+        lift = _upload(dc, lift)
+        F -= dc.apply(lift, _lib.PLAIN)
+    dc.zero_dirichlet(F)
+    return F, lift
+
+
+def apply_element_inverse(Fu, Fq, ctx):
+    """Interior block inverse of stacked (u, q1, q2, q3) element data by fast diagonalisation
+    (solver.py:129-155), on the device (hdgb_element_inverse).  Inputs (ne, n, n, n); returns
+    (u, (q1, q2, q3)) as new numpy arrays (CUDA tensors if Fu is one)."""
+    import ctypes
+
+    import torch
+
+    dc = device_context(ctx)
+    ne, n = ctx.mesh.n_elements, ctx.basis.n
+    shape = (ne, n, n, n)
+    as_t = isinstance(Fu, torch.Tensor)
+    fu = _upload(dc, Fu).reshape(-1)
+    fq = torch.stack([_upload(dc, q).reshape(shape) for q in Fq]).reshape(-1)
+    if fu.numel() != ne * n ** 3 or fq.numel() != 3 * ne * n ** 3:
+        raise ValueError("element arrays must have shape (n_elements, p+1, p+1, p+1)")
+    u = torch.empty_like(fu)
+    q = torch.empty_like(fq)
+    _lib.check(_lib.lib().hdgb_element_inverse(dc.handle, ctypes.c_void_p(fu.data_ptr()), ctypes.c_void_p(fq.data_ptr()),
+                                               ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(q.data_ptr()),
+                                               dc.stream()))
+    _count(ctx, _inverse_ops(ctx))
+    qs = [q[d * ne * n ** 3:(d + 1) * ne * n ** 3].view(shape) for d in range(3)]
+    if as_t:
+        return u.view(shape), tuple(qs)
+    u, *qs = dc.download([u.view(shape), *qs])
+    return u, tuple(qs)
+
+
+def hybridize_initial_guess(u, ctx, g_D=None, g_N=None):
+    """Trace consistent with an interior field u (solver.py:158-195), on the device
+    (hdgb_hybridize); Dirichlet faces take g_D.  Returns a new FluxField."""
+    dc = device_context(ctx)
+    mesh, p = ctx.mesh, ctx.basis.p
+    gN = _kind_faces(ctx, g_N, NEUMANN)
+    x = dc.hybridize(u, None if gN is None else _upload(dc, gN))
+    field = _field(mesh, p, dc.download([x])[0])
+    if g_D is not None:
+        _restore_dirichlet(field, g_D)
+    return field
+
+
+def build_rhs(f, g_D, g_N, ctx):
+    """Condensed right-hand side with Neumann data and Dirichlet lift (solver.py:212-251), on the
+    device; Dirichlet slots are zero.  Returns a new FluxField."""
+    dc = device_context(ctx)
+    F, lift = _device_rhs(ctx, dc, _upload(dc, f), g_D, g_N)
+    mesh, p = ctx.mesh, ctx.basis.p
+    n = p + 1
+    _count(ctx, _inverse_ops(ctx) + 24 * mesh.n_elements * n ** 3
+           + (mesh.n_elements * (73 * n ** 3 + 12 * n ** 2) if lift is not None else 0))
+    return _field(mesh, p, dc.download([F])[0])
+
+
+def recover_interior(f, u_tilde, ctx):
+    """Interior solution and gradient from a trace field (solver.py:254-279), on the device
+    (hdgb_recover_interior).  Returns (u, (q1, q2, q3)) as new numpy arrays."""
+    dc = device_context(ctx)
+    tr = _upload(dc, _all_faces(u_tilde))
+    if tr.numel() != dc.n_all:
+        raise ValueError("trace field has the wrong size")
+    u, qs = dc.recover_interior(_upload(dc, f), tr)
+    n = ctx.basis.n
+    _count(ctx, _inverse_ops(ctx) + 24 * ctx.mesh.n_elements * n ** 3)
+    u, *qs = dc.download([u, *qs])
+    return u, tuple(qs)
 
 
 def _build_preconditioner(kind, ctx):
@@ -531,32 +483,9 @@ def _solve_device(u0, f, g_D, g_N, cfg, ctx, transformed):
     dev = f"cuda:{dc.device}"
     counter = getattr(ctx, "counter", None)
     fd = torch.as_tensor(np.ascontiguousarray(f), dtype=torch.float64).to(dev)  # uploaded once: RHS and recovery
-    F = dc.build_rhs(fd)
-    if g_N is not None:  # Neumann data (solver.py:233-237)
-        neu = FluxField(mesh, p)
-        for d in range(3):
-            m = mesh.face_kind[d] == NEUMANN
-            if np.any(m):
-                fm = _face_mass(ctx, d)
-                neu.data[d][m] = (fm[0] if fm.shape[0] == 1 else fm[m]) * g_N.data[d][m]
-        F += torch.from_numpy(pack_all(neu)).to(dev)
-    lift = None
-    if g_D is not None:  # Dirichlet lift (solver.py:239-249)
-        lf = FluxField(mesh, p)
-        for d in range(3):
-            m = mesh.face_kind[d] == DIRICHLET
-            lf.data[d][m] = g_D.data[d][m]
-        if any(np.any(x) for x in lf.data):
-            lift = torch.from_numpy(pack_all(lf)).to(dev)
-            F -= dc.apply(lift, _lib.PLAIN)
-    dc.zero_dirichlet(F)
-    gN = None
-    if g_N is not None:
-        gf = FluxField(mesh, p)
-        for d in range(3):
-            m = mesh.face_kind[d] == NEUMANN
-            gf.data[d][m] = g_N.data[d][m]
-        gN = torch.from_numpy(pack_all(gf)).to(dev)
+    F, lift = _device_rhs(ctx, dc, fd, g_D, g_N)
+    gN = _kind_faces(ctx, g_N, NEUMANN)
+    gN = None if gN is None else _upload(dc, gN)
     x = dc.hybridize(u0, gN)  # Dirichlet slots 0: the PCG keeps them there, the lift restores them
     if transformed:  # Alg. 6: solve in the eigenbasis (solver.py:381-399)
         F = dc.zero_dirichlet(dc.transform(F, np.ascontiguousarray(ctx.basis.S.T)))
@@ -591,52 +520,6 @@ def solve(u0, f, g_D, g_N, cfg, ctx):
     return _solve_device(u0, f, g_D, g_N, cfg, ctx, False)
 
 
-def solve_host_pipeline(u0, f, g_D, g_N, cfg, ctx):
-    """solve() with the host pre/post restatements around the device PCG (parity reference)."""
-    if cfg.preconditioner == "transformed":
-        return solve_transformed_host_pipeline(u0, f, g_D, g_N, cfg, ctx)
-    ops0 = _ops(ctx)
-    prec = _build_preconditioner(cfg.preconditioner, ctx)
-    u_tilde0 = hybridize_initial_guess(u0, ctx, g_D, g_N)
-    F = build_rhs(f, g_D, g_N, ctx)
-    mesh, p = ctx.mesh, ctx.basis.p
-    apply_K = DeviceOperator(ctx, _lib.PLAIN)
-    apply_P = prec.apply_packed if prec is not None else None
-    t0 = time.perf_counter()
-    x, iters, relres, conv = pcg(apply_K, apply_P, pack_unknowns(F), pack_unknowns(u_tilde0), cfg.rtol, cfg.atol,
-                                 cfg.max_iters)
-    wall = time.perf_counter() - t0
-    flux = unpack_unknowns(x, mesh, p)
-    _restore_dirichlet(flux, g_D)
-    u, qs = recover_interior(f, flux, ctx)
-    ops1 = _ops(ctx)
-    return u, qs, SolveReport(iters, relres, conv, wall, wall / max(iters, 1),
-                              None if ops0 is None else ops1 - ops0)
-
-
 def solve_transformed(u0, f, g_D, g_N, cfg, ctx):
     """Same pipeline in the transformed basis (solver.py:372-410, Alg. 6)."""
     return _solve_device(u0, f, g_D, g_N, cfg, ctx, True)
-
-
-def solve_transformed_host_pipeline(u0, f, g_D, g_N, cfg, ctx):
-    """solve_transformed() with the host pre/post restatements (parity reference)."""
-    ops0 = _ops(ctx)
-    prec = transformed_preconditioner(ctx)
-    u_tilde0 = hybridize_initial_guess(u0, ctx, g_D, g_N)
-    F = build_rhs(f, g_D, g_N, ctx)
-    mesh, p = ctx.mesh, ctx.basis.p
-    S = ctx.basis.S
-    F_hat = transform_faces(F, S.T, ctx.counter, ctx=ctx).zero_dirichlet()
-    x0_hat = transform_faces(u_tilde0, ctx.T, ctx.counter, ctx=ctx)
-    apply_K = DeviceOperator(ctx, _lib.TRANSFORMED)
-    t0 = time.perf_counter()
-    x, iters, relres, conv = pcg(apply_K, prec.apply_packed, pack_unknowns(F_hat), pack_unknowns(x0_hat), cfg.rtol,
-                                 cfg.atol, cfg.max_iters)
-    wall = time.perf_counter() - t0
-    flux = transform_faces(unpack_unknowns(x, mesh, p), S, ctx.counter, ctx=ctx)
-    _restore_dirichlet(flux, g_D)
-    u, qs = recover_interior(f, flux, ctx)
-    ops1 = _ops(ctx)
-    return u, qs, SolveReport(iters, relres, conv, wall, wall / max(iters, 1),
-                              None if ops0 is None else ops1 - ops0)

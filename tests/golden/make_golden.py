@@ -215,7 +215,80 @@ def case_nonuniform():
                         tau_hat=tau_hat, u_all=u_all, K_u_all=K @ u_all, y_all=y, S=b.S, B_S=b.B_S)
 
 
+def _fluxfield_on(mesh, p, kind, rng):
+    """Seeded face data on the faces of one kind (zero elsewhere)."""
+    fld = H.FluxField(mesh, p)
+    for d in range(3):
+        m = mesh.face_kind[d] == kind
+        fld.data[d][m] = rng.uniform(-1.0, 1.0, fld.data[d][m].shape)
+    return fld
+
+
+def case_prepost():
+    """The solve's element-local pre/post steps and whole solves (solver.py:129-410), from the
+    reference, plus the reference test-suite's monolithic dense LDG solves
+    (pkg/tests/dense_oracles.py:113-164) of its test_pcg_matches_dense_solve and
+    test_neumann_problem_matches_monolithic problems (pkg/tests/test_solver.py:232-239, 317-336)."""
+    from dense_oracles import monolithic_solve
+    from test_solver import TWO_PI, make_problem, smooth_f, smooth_u
+
+    from hdgbox.harness import dirichlet_data
+    from hdgbox.solver import apply_element_inverse, hybridize_initial_guess, recover_interior
+
+    d = {}
+    # (a) pre/post pieces on the mixed-BC, non-cubic grid (reference tau convention)
+    bc = ("dirichlet", "neumann", "neumann", "dirichlet", "dirichlet", "neumann")
+    mesh = H.Mesh((3, 2, 2), (0, 0, 0), (1.5, 2.0, 1.0), bc)
+    p, lam = 3, 1.7
+    ctx = H.make_context(mesh, p, H.SolverConfig(lam=lam, tau=2.0, tau_convention="reference"))
+    n = p + 1
+    shape = (mesh.n_elements, n, n, n)
+    rng = np.random.default_rng(41)
+    u0 = rng.uniform(-1.0, 1.0, shape)
+    f = rng.uniform(-1.0, 1.0, shape)
+    g_D = _fluxfield_on(mesh, p, H.DIRICHLET, rng)
+    g_N = _fluxfield_on(mesh, p, H.NEUMANN, rng)
+    trace = unpack_all(rng.uniform(-1.0, 1.0, sum(mesh.n_faces) * n * n), mesh, p)
+    Fu = rng.uniform(-1.0, 1.0, shape)
+    Fq = tuple(rng.uniform(-1.0, 1.0, shape) for _ in range(3))
+    d.update(mix_u0=u0, mix_f=f, mix_gD=pack_all(g_D), mix_gN=pack_all(g_N), mix_trace=pack_all(trace), mix_Fu=Fu,
+             mix_Fq=np.stack(Fq), tau_hat=ctx.basis.tau_hat)
+    d["mix_hyb"] = pack_all(hybridize_initial_guess(u0, ctx, g_D, g_N))
+    d["mix_rhs"] = pack_all(build_rhs(f, g_D, g_N, ctx))
+    u, qs = recover_interior(f, trace, ctx)
+    d["mix_rec_u"], d["mix_rec_q"] = u, np.stack(qs)
+    w, qw = apply_element_inverse(Fu, Fq, ctx)
+    d["mix_inv_u"], d["mix_inv_q"] = w, np.stack(qw)
+    for name, prec in (("block", "block"), ("trans", "transformed")):
+        cfg = H.SolverConfig(lam=lam, tau=2.0, tau_convention="reference", preconditioner=prec, rtol=1e-12)
+        us, qss, rep = H.solve(u0, f, g_D, g_N, cfg, ctx)
+        d[f"mix_solve_{name}_u"], d[f"mix_solve_{name}_q"] = us, np.stack(qss)
+        d[f"mix_solve_{name}_it"] = rep.iterations
+    # (b) test_pcg_matches_dense_solve: all-Dirichlet, p = 3, lambda = 0 on [0, 2 pi]^3
+    mesh, cfg, ctx, f, g_D, _ = make_problem(p=3, lam=0.0, rtol=1e-12)
+    u_m, q_m, _ = monolithic_solve(ctx.basis, mesh, 0.0, f, g_D)
+    d.update(dense_f=f, dense_gD=pack_all(g_D), dense_u=u_m, dense_q=np.stack(q_m))
+    # (c) test_neumann_problem_matches_monolithic: x1-high Neumann side, lambda = 0.5
+    bcn = ("dirichlet", "neumann", "dirichlet", "dirichlet", "dirichlet", "dirichlet")
+    mesh = H.Mesh((2, 2, 2), (0.0, 0.0, 0.0), (TWO_PI,) * 3, bcn)
+    ctx = H.make_context(mesh, 3, H.SolverConfig(lam=0.5, tau=25.0, rtol=1e-12))
+    b = ctx.basis
+    f = element_field(mesh, b, smooth_f(0.5))
+    g_D = dirichlet_data(mesh, b, smooth_u)
+    g_N = H.FluxField(mesh, 3)
+    m = mesh.face_kind[0] == H.NEUMANN
+    X1, X2, X3 = mesh.face_node_grids(0, b.nodes)
+    g_N.data[0][m] = np.broadcast_to(np.cos(X1) * np.sin(X2) * np.sin(X3), g_N.data[0].shape)[m]
+    u_m, q_m, _ = monolithic_solve(b, mesh, 0.5, f, g_D, g_N)
+    d.update(neu_f=f, neu_gD=pack_all(g_D), neu_gN=pack_all(g_N), neu_u=u_m, neu_q=np.stack(q_m))
+    np.savez_compressed(os.path.join(OUT, "prepost.npz"), **d)
+
+
 if __name__ == "__main__":
-    for fn in (case_cfg1, case_mixed, case_psweep, case_nonuniform, case_cfg2):
+    if sys.argv[1:] == ["prepost"]:
+        case_prepost()
+        print("wrote case_prepost")
+        sys.exit(0)
+    for fn in (case_cfg1, case_mixed, case_psweep, case_nonuniform, case_cfg2, case_prepost):
         fn()
         print("wrote", fn.__name__)

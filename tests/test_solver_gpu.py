@@ -1,4 +1,10 @@
-"""End-to-end solve()/solve_transformed() on the device (pre/post on the host)."""
+"""End-to-end solve()/solve_transformed() and the pre/post steps on the device.
+
+Checked against the reference's own outputs (tests/golden/prepost.npz: hybridize_initial_guess,
+build_rhs, recover_interior, apply_element_inverse and whole solves from hdgbox, plus the
+reference test-suite's monolithic dense LDG solves) and against the host restatement
+(oracle/host_prepost.py) on grids the reference cannot express (non-uniform widths).
+"""
 import numpy as np
 import pytest
 
@@ -6,6 +12,8 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_2007_11891_b200 as hb  # noqa: E402
+from oracle import host_prepost as HP  # noqa: E402
+from tests._golden import load, relerr  # noqa: E402
 
 TWO_PI = 2.0 * np.pi
 
@@ -86,12 +94,12 @@ def test_device_build_rhs_and_recover_match_host(p, bc, lam):
     dc = hb.device_context(ctx)
     rng = np.random.default_rng(p)
     f = rng.uniform(-1, 1, (mesh.n_elements,) + (ctx.basis.n,) * 3)
-    F_host = hb.pack_all(hb.build_rhs(f, None, None, ctx))
+    F_host = hb.pack_all(HP.build_rhs(f, None, None, ctx))
     F_dev = dc.build_rhs(f)
     dc.zero_dirichlet(F_dev)
     assert np.max(np.abs(F_dev.cpu().numpy() - F_host)) <= 1e-12 * np.max(np.abs(F_host))
     tr = rng.uniform(-1, 1, mesh.n_all(p))
-    u_h, q_h = hb.recover_interior(f, hb.unpack_all(tr, mesh, p), ctx)
+    u_h, q_h = HP.recover_interior(f, hb.unpack_all(tr, mesh, p), ctx)
     u_d, q_d = dc.recover_interior(f, torch.from_numpy(tr).cuda())
     assert np.max(np.abs(u_d.cpu().numpy() - u_h)) <= 1e-12 * np.max(np.abs(u_h))
     for d in range(3):
@@ -124,11 +132,11 @@ def test_device_pre_post_nonuniform_grid():
     ctx = hb.OperatorContext(hb.Basis1D(p, 0.4), mesh, 2.0)
     dc = hb.device_context(ctx)
     f = rng.uniform(-1, 1, (mesh.n_elements,) + (p + 1,) * 3)
-    F_host = hb.pack_all(hb.build_rhs(f, None, None, ctx))
+    F_host = hb.pack_all(HP.build_rhs(f, None, None, ctx))
     F_dev = dc.zero_dirichlet(dc.build_rhs(f))
     assert np.max(np.abs(F_dev.cpu().numpy() - F_host)) <= 1e-12 * np.max(np.abs(F_host))
     tr = rng.uniform(-1, 1, mesh.n_all(p))
-    u_h, q_h = hb.recover_interior(f, hb.unpack_all(tr, mesh, p), ctx)
+    u_h, q_h = HP.recover_interior(f, hb.unpack_all(tr, mesh, p), ctx)
     u_d, q_d = dc.recover_interior(f, torch.from_numpy(tr).cuda())
     assert np.max(np.abs(u_d.cpu().numpy() - u_h)) <= 1e-12 * np.max(np.abs(u_h))
     for d in range(3):
@@ -141,7 +149,7 @@ def test_device_resident_solve_matches_host_pipeline(precond):
     mesh, cfg, ctx, f, g_D, _ = make_problem(p=5, lam=0.5, precond=precond)
     u0 = np.random.default_rng(2).uniform(-1, 1, (mesh.n_elements,) + (ctx.basis.n,) * 3)
     u_d, q_d, rd = hb.solve(u0, f, g_D, None, cfg, ctx)
-    u_h, q_h, rh = hb.solve_host_pipeline(u0, f, g_D, None, cfg, ctx)
+    u_h, q_h, rh = HP.solve_host_pipeline(u0, f, g_D, None, cfg, ctx)
     assert rd.converged and abs(rd.iterations - rh.iterations) <= 1
     assert np.max(np.abs(u_d - u_h)) <= 1e-8 * np.max(np.abs(u_h))
     for d in range(3):
@@ -167,7 +175,7 @@ def test_device_hybridize_matches_host(uniform):
     g_N = hb.FluxField(mesh, p)
     for d in range(3):
         g_N.data[d][...] = rng.uniform(-1, 1, g_N.data[d].shape)
-    host = hb.hybridize_initial_guess(u0, ctx, None, g_N)
+    host = HP.hybridize_initial_guess(u0, ctx, None, g_N)
     hv = hb.pack_all(host)
     gn_all = hb.FluxField(mesh, p)
     for d in range(3):
@@ -195,7 +203,7 @@ def test_device_resident_solve_with_neumann_data_matches_host_pipeline():
         g_N.data[d][m] = rng.uniform(-0.5, 0.5, g_N.data[d][m].shape)
     u0 = np.zeros((mesh.n_elements,) + (b.n,) * 3)
     u_d, q_d, rd = hb.solve(u0, f, g_D, g_N, cfg, ctx)
-    u_h, q_h, rh = hb.solve_host_pipeline(u0, f, g_D, g_N, cfg, ctx)
+    u_h, q_h, rh = HP.solve_host_pipeline(u0, f, g_D, g_N, cfg, ctx)
     assert rd.converged and abs(rd.iterations - rh.iterations) <= 1
     assert np.max(np.abs(u_d - u_h)) <= 1e-8 * np.max(np.abs(u_h))
     for d in range(3):
@@ -208,3 +216,101 @@ def test_device_solve_reports_reference_flop_totals():
     u0 = np.zeros((mesh.n_elements,) + (ctx.basis.n,) * 3)
     _, _, rep = hb.solve(u0, f, g_D, None, cfg, ctx_c)
     assert rep.flops == hb.solve_flop_count(mesh, 3, rep.iterations, False, True) == ctx_c.counter.ops
+
+
+# ---------------------------------------------------------------- pinned to the reference (prepost.npz)
+def _mixed_ctx(g):
+    bc = ("dirichlet", "neumann", "neumann", "dirichlet", "dirichlet", "neumann")
+    mesh = hb.Mesh((3, 2, 2), (0, 0, 0), (1.5, 2.0, 1.0), bc)
+    ctx = hb.make_context(mesh, 3, hb.SolverConfig(lam=1.7, tau=2.0, tau_convention="reference"))
+    assert ctx.basis.tau_hat == float(g["tau_hat"])
+    return mesh, ctx
+
+
+@pytest.mark.parametrize("impl", ["device", "host"])
+def test_prepost_steps_match_reference(impl):
+    """hybridize_initial_guess, build_rhs (Neumann data + Dirichlet lift), recover_interior and
+    apply_element_inverse against the reference's outputs (solver.py:129-279); the public
+    functions run on the device, the host restatement is the checker."""
+    g = load("prepost")
+    mesh, ctx = _mixed_ctx(g)
+    p = 3
+    m = hb if impl == "device" else HP
+    g_D, g_N = hb.unpack_all(g["mix_gD"], mesh, p), hb.unpack_all(g["mix_gN"], mesh, p)
+    assert relerr(hb.pack_all(m.hybridize_initial_guess(g["mix_u0"], ctx, g_D, g_N)), g["mix_hyb"]) < 1e-12
+    assert relerr(hb.pack_all(m.build_rhs(g["mix_f"], g_D, g_N, ctx)), g["mix_rhs"]) < 1e-12
+    u, qs = m.recover_interior(g["mix_f"], hb.unpack_all(g["mix_trace"], mesh, p), ctx)
+    assert relerr(u, g["mix_rec_u"]) < 1e-12
+    for d in range(3):
+        assert relerr(qs[d], g["mix_rec_q"][d]) < 1e-12
+    w, qw = m.apply_element_inverse(g["mix_Fu"], tuple(g["mix_Fq"]), ctx)
+    assert relerr(w, g["mix_inv_u"]) < 1e-12
+    for d in range(3):
+        assert relerr(qw[d], g["mix_inv_q"][d]) < 1e-12
+
+
+@pytest.mark.parametrize("name,prec", [("block", "block"), ("trans", "transformed")])
+def test_solve_with_mixed_data_matches_reference_solve(name, prec):
+    """Whole solve (u0 != 0, inhomogeneous Dirichlet and Neumann data) against hdgbox.solve."""
+    g = load("prepost")
+    mesh, _ = _mixed_ctx(g)
+    cfg = hb.SolverConfig(lam=1.7, tau=2.0, tau_convention="reference", preconditioner=prec, rtol=1e-12)
+    ctx = hb.make_context(mesh, 3, cfg)
+    g_D, g_N = hb.unpack_all(g["mix_gD"], mesh, 3), hb.unpack_all(g["mix_gN"], mesh, 3)
+    u, qs, rep = hb.solve(g["mix_u0"], g["mix_f"], g_D, g_N, cfg, ctx)
+    assert rep.converged and abs(rep.iterations - int(g[f"mix_solve_{name}_it"])) <= 1
+    assert relerr(u, g[f"mix_solve_{name}_u"]) < 1e-9
+    for d in range(3):
+        assert relerr(qs[d], g[f"mix_solve_{name}_q"][d]) < 1e-9
+
+
+@pytest.mark.parametrize("prec", ["block", "transformed"])
+def test_solve_matches_monolithic_dense_solve(prec):
+    """The reference's test_pcg_matches_dense_solve (pkg/tests/test_solver.py:232-239): the device
+    solve against the monolithic dense LDG solve of dense_oracles.py:113-164."""
+    g = load("prepost")
+    mesh = hb.Mesh((2, 2, 2), (0.0, 0.0, 0.0), (TWO_PI,) * 3, "dirichlet")
+    cfg = hb.SolverConfig(lam=0.0, rtol=1e-12, preconditioner=prec)
+    ctx = hb.make_context(mesh, 3, cfg)
+    g_D = hb.unpack_all(g["dense_gD"], mesh, 3)
+    u, qs, rep = hb.solve(np.zeros_like(g["dense_f"]), g["dense_f"], g_D, None, cfg, ctx)
+    assert rep.converged and rep.relative_residual <= cfg.rtol
+    assert np.max(np.abs(u - g["dense_u"])) <= 1e-8
+    for d in range(3):
+        assert np.max(np.abs(qs[d] - g["dense_q"][d])) <= 1e-7
+
+
+def test_neumann_solve_matches_monolithic_dense_solve():
+    """The reference's test_neumann_problem_matches_monolithic (pkg/tests/test_solver.py:317-336)."""
+    g = load("prepost")
+    bc = ("dirichlet", "neumann", "dirichlet", "dirichlet", "dirichlet", "dirichlet")
+    mesh = hb.Mesh((2, 2, 2), (0.0, 0.0, 0.0), (TWO_PI,) * 3, bc)
+    cfg = hb.SolverConfig(lam=0.5, tau=25.0, rtol=1e-12)
+    ctx = hb.make_context(mesh, 3, cfg)
+    g_D, g_N = hb.unpack_all(g["neu_gD"], mesh, 3), hb.unpack_all(g["neu_gN"], mesh, 3)
+    u, _, rep = hb.solve(np.zeros_like(g["neu_f"]), g["neu_f"], g_D, g_N, cfg, ctx)
+    assert rep.converged
+    assert np.max(np.abs(u - g["neu_u"])) <= 1e-8
+
+
+def test_single_face_system_solved_in_one_iteration():
+    """The reference's test_single_face_system_solved_in_one_iteration
+    (pkg/tests/test_preconditioner.py:65-78): (2,1,1) all-Dirichlet, the only unknowns live on one
+    interior face, so the block preconditioner is the exact inverse - fused device PCG."""
+    mesh = hb.Mesh((2, 1, 1))
+    ctx = hb.OperatorContext(hb.Basis1D(2, 1.0), mesh, 0.0)
+    F = np.random.default_rng(0).standard_normal(mesh.n_trace_unknowns(2))
+    x, iters, relres, conv = hb.pcg(hb.DeviceOperator(ctx, 0), hb.build_block_preconditioner(ctx).apply_packed, F,
+                                    np.zeros_like(F), rtol=1e-10)
+    assert conv and iters == 1
+
+
+def test_direct_fused_pcg_counts_operator_flops():
+    """pcg(DeviceOperator(ctx), ...) on the fused path adds the K applies the reference's apply_K
+    closure would count (operator.py:47-68): (iterations + 1) n_e (73 n^3 + 12 n^2)."""
+    mesh = hb.Mesh((3, 3, 2))
+    ctx = hb.OperatorContext(hb.Basis1D(4, 1.0), mesh, 0.5, hb.FlopCounter())
+    F = np.random.default_rng(1).standard_normal(mesh.n_trace_unknowns(4))
+    x, it, rel, conv = hb.pcg(hb.DeviceOperator(ctx, 0), hb.build_block_preconditioner(ctx).apply_packed, F,
+                              np.zeros_like(F))
+    assert conv and ctx.counter.ops == (it + 1) * mesh.n_elements * (73 * 5 ** 3 + 12 * 5 ** 2)
