@@ -467,6 +467,65 @@ def _distributed_cg(dc, halo, mesh, N, N_all, n, rank, world, stream):
     return cg
 
 
+def _config5_xsplit(hb, rank, world, local, stream, flush, steps=5):
+    """BASELINE configs[4] strong scaling: the 128^3, p = 8, lambda = 1 grid split along x over the
+    ranks (distributed.slab_mesh / slab_side_kinds), one operator apply + NCCL halo exchange per
+    step and a 10-iteration distributed block PCG (distributed.SlabSystem); device times, max over
+    ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2007_11891_b200.distributed import SlabHalo, SlabSystem, slab_mesh, slab_side_kinds
+
+    gn, p, lam = (128, 128, 128), 8, 1.0
+    mesh = slab_mesh(gn, (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), rank, world)
+    basis = hb.Basis1D(p, 25.0 * (1.0 / 128) / 2.0)
+    dc = hb.DeviceContext(basis, mesh, lam, device=local, side_kinds=slab_side_kinds(rank, world))
+    halo = SlabHalo(dc, rank, world)
+    gen = torch.Generator(device="cuda").manual_seed(5 + rank)
+    u = torch.rand(dc.n_all, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    dc.zero_dirichlet(u)
+    r = dc.empty()
+
+    def step():
+        dc.apply(u, 0, out=r)
+        halo.exchange_add(r)
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b) * 1e-3)
+        t = torch.tensor([statistics.median(ts)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    N_glob = hb.Mesh(gn).n_trace_unknowns(p)
+    t_apply = timed(step, steps)
+    sysm = SlabSystem(dc, halo, variant=0, prec=1)
+    F = u.clone()
+    x0 = torch.zeros_like(F)
+    t_cg = timed(lambda: sysm.solve(F, x0, rtol=1e-300, max_iters=10), 2) / 10
+    out = {"workload": "BASELINE configs[4]: 128^3 elements, p=8, lambda=1, split along x over the GPUs",
+           "scaling": "strong", "trace_unknowns": N_glob, "apply_ms": t_apply * 1e3,
+           "trace_dof_per_s": N_glob / t_apply, "pcg_ms_per_iter": t_cg * 1e3,
+           "ps_per_unknown_per_iter": t_cg / N_glob * 1e12,
+           "note": "apply = local element passes + NCCL halo exchange of the interface x-face planes; PCG = "
+                   "distributed.SlabSystem (host-driven recurrence, two allreduces per iteration)"}
+    del dc, u, r, F, x0
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -479,6 +538,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     p, n = CFG["p"], CFG["p"] + 1
+    large = {}
     if world > 1:
         import paper_2007_11891_b200 as hb
         from paper_2007_11891_b200.distributed import slab_mesh, slab_side_kinds
@@ -667,6 +727,10 @@ def run_ours(args):
             cg = _distributed_cg(dc, halo, mesh, N, N_all, n, rank, world, stream)
         except Exception as exc:  # keep the apply line even if the solve fails on this box
             cg = {"error": f"{type(exc).__name__}: {exc}"}
+        try:
+            large["config5_xsplit"] = _config5_xsplit(hb, rank, world, local, stream, flush)
+        except Exception as exc:
+            large["config5_xsplit"] = {"error": f"{type(exc).__name__}: {exc}"}
 
     # ---- end-to-end solve() (public API, device-resident pre/post + fused PCG), config 2
     solve_rec = None
@@ -715,7 +779,6 @@ def run_ours(args):
             "flops": "reference FlopCounter: n_e(73n^3+12n^2) plain, n_e(25n^3+12n^2) transformed"}
 
     # ---- large single-GPU workloads (BASELINE configs[2] p-sweep, ~2e7 unknowns; config 5)
-    large = {}
     if world == 1 and not args.no_large:
         sizes = {2: 91, 3: 75, 4: 65, 6: 52, 8: 44, 12: 34, 16: 29}
         ps = [2, 3, 4, 6, 8, 12, 16] if args.sweep else [8]

@@ -94,6 +94,8 @@ def lib():
                 "(there is no CPU fallback for the hot path)")
         L = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("HDGB_LIB") and not hasattr(L, name):
+                continue  # an older side build (A/B timing) may lack newer entry points
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

@@ -96,7 +96,10 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
   c->dev = d->device;
   if (const char* sb = getenv("HDGB_SLAB_MB")) c->slab_bytes = (int64_t)atof(sb) * (1LL << 20);
   if (const char* gc = getenv("HDGB_GRID_CAP")) c->grid_cap = atoll(gc);
+  c->merge = d->p + 1 >= 17;
   if (const char* mg = getenv("HDGB_MERGE")) c->merge = atoi(mg);
+  if (const char* ms = getenv("HDGB_MERGE_SLACK")) c->merge_slack = atoi(ms);
+  if (const char* mb = getenv("HDGB_MERGE_BATCH")) c->merge_batch = atoi(mb) > 0 ? atoi(mb) : 1;
   if (cudaSetDevice(c->dev) != cudaSuccess) {
     delete c;
     return einval("invalid CUDA device");

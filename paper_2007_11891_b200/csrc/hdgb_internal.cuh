@@ -127,7 +127,9 @@ struct OpArgs {
   double* xout;          // CG mode, fused direction update: x (deferred x += alpha_prev p_prev)
   uint32_t* wdone;       // merged colour schedule: per-wave colour-0 arrivals (+ exit ticket)
   int64_t wcount;        //   waves per colour
-  int64_t wlag;          //   colour-0 waves ahead of colour-1 wave 0
+  int64_t wlag;          //   colour-0 waves ahead of colour-1 wave 0 (placement)
+  int64_t wdep;          //   colour-0 waves a colour-1 wave depends on beyond its own index
+  int64_t wbatch;        //   colour-0 waves per arrival counter
 };
 
 struct FaceArgs {
@@ -322,10 +324,15 @@ struct hdgb_ctx {
   // ring; 0 = the resident grid
   int64_t grid_cap = 0;
   // merged colour schedule of the element kernel (both passes in one launch, L2-ordered):
-  // per-wave arrival counters (npairs + 2 words, zero between launches); HDGB_MERGE=0 runs the
-  // two colour passes as separate launches
+  // per-wave arrival counters (npairs + 2 words, zero between launches).  Measured on config 3:
+  // DRAM traffic of the pair at p = 8 drops from 732 to 404 MB (algorithmic 324 MB), but the
+  // LSU-bound element kernel runs slower merged (p = 8 257 -> 307 us, p = 2 210 -> 238 us) and
+  // faster only at N = 17 (p = 16 460 -> 426 us), so it is the default there; HDGB_MERGE=0/1
+  // forces either schedule
   uint32_t* d_wdone = nullptr;
   int merge = 1;
+  int merge_slack = 4;  // extra colour-0 waves of lead (CTA drift) beyond the neighbour dependency
+  int merge_batch = 4;  // colour-0 waves per arrival (one fence + atomic per batch and CTA)
 };
 
 namespace hdgb {

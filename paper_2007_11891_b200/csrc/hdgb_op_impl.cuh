@@ -143,7 +143,21 @@ struct OpVCfg {
   static constexpr bool TMA = N >= HDGB_OPV_TMA_NMIN && N <= HDGB_OPV_TMA_NMAX;
   static constexpr int FSTR = (TMA && (NQ & 1)) ? NQ + 1 : NQ;  // face slot stride
   static constexpr int FS = 6 * FSTR;                   // staged faces of one element
-  static constexpr int VS = N * NQ;                     // U volume of one element
+  // U volume of one element: U(a1, a2, a3) at a1 S1 + a2 S2 + a3 S3.  Phase 1 stores (a2, a3)
+  // across the lanes, phase 2 reads (a1, a3) (y faces) and (a1, a2) (z faces); the strides are the
+  // bank-conflict minimum over the three access patterns (64-bit accesses, 16 lanes per
+  // wavefront; exhaustive search over axis order and padding): for even N the natural
+  // a3-fastest layout conflicts up to 6-fold (N = 16: 288 wavefronts per 3 passes instead of
+  // 48; N = 8: 44 instead of 16), an a2-fastest layout with an a3 plane padding of 1 (N = 0 mod 4)
+  // or 5 (N = 2 mod 4) reaches 48 / 16; N = 4 takes a1-fastest with a padding of 3; odd N keep
+  // a3-fastest, at or near the minimum (N = 3: 4 vs 3, measured slower re-laid).  Measured on
+  // config 3: p = 3 transformed apply 181 -> 169 us, p = 7 (40^3) 149 -> 134 us.
+  static constexpr int VPAD = (N & 3) == 0 ? 1 : 5;
+  static constexpr bool VEVEN = N >= 6 && !(N & 1);
+  static constexpr int S1 = VEVEN ? N : (N == 4 ? 1 : NQ);
+  static constexpr int S2 = VEVEN ? 1 : N;
+  static constexpr int S3 = VEVEN ? NQ + VPAD : (N == 4 ? NQ + 3 : 1);
+  static constexpr int VS = VEVEN ? N * (NQ + VPAD) : (N == 4 ? N * (NQ + 3) : N * NQ);
   // dz_inv lines in registers (N values per thread) up to N = 11; from a shared copy of the
   // table for N >= 12, where the registers are worth more (measured: p = 12 339 -> 312 us,
   // p = 16 490 -> 433 us; slower below)
@@ -389,7 +403,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     int64_t gi_unused, wave;
     slot_item(k, col, gi_unused, wave);
     if (COLOR == 2 && col == 1 && tid == 0) {  // the colour-0 neighbours of this wave are complete
-      const int64_t need = min((int64_t)a.wcount - 1, wave + (int64_t)a.wlag - 1);
+      const int64_t need = min((int64_t)a.wcount - 1, wave + (int64_t)a.wdep) / a.wbatch;  // last batch needed
       for (int64_t v = verified + 1; v <= need; ++v)
         while (ld_acquire_u32(a.wdone + v) < gridDim.x) {
         }
@@ -464,7 +478,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
         const double dzv = DZR ? dzr[DZR ? a1 : 0]
                                : (UNI ? sDz[a1 * NQ + q] : __drcp_rn(fma(al1, K.Lam[a1], base)));  // EigenScale3D
         const double U = F * dzv;
-        vU[a1 * NQ + q] = U;
+        vU[a1 * C::S1 + qa * C::S2 + qb * C::S3] = U;
         ax0 = fma(K.B0[a1], U, ax0);
         ax1 = fma(K.B1[a1], U, ax1);
       }
@@ -473,12 +487,12 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     }
     __syncthreads();
     if (on) {  // phase 2: y faces at (a1, a3) = (qa, qb), z faces at (a1, a2) = (qa, qb)
-      const double* col = vU + qa * NQ + qb;      // over a2, stride N
-      const double* row = vU + qa * NQ + qb * N;  // over a3, contiguous
+      const double* ycol = vU + qa * C::S1 + qb * C::S3;  // over a2
+      const double* zrow = vU + qa * C::S1 + qb * C::S2;  // over a3
       double ay0 = 0.0, ay1 = 0.0, az0 = 0.0, az1 = 0.0;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        const double vy = col[k * N], vz = row[k];
+        const double vy = ycol[k * C::S2], vz = zrow[k * C::S3];
         ay0 = fma(K.B0[k], vy, ay0);
         ay1 = fma(K.B1[k], vy, ay1);
         az0 = fma(K.B0[k], vz, az0);
@@ -491,9 +505,9 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       emit(5, al3 * az1, al3 * zr1, zr1);
     }
     __syncthreads();  // staging buffer, volume and element info are reused
-    if (COLOR == 2 && col == 0 && tid == 0) {  // this CTA's colour-0 group of the wave is stored
-      __threadfence();
-      atomicAdd(a.wdone + wave, 1u);
+    if (COLOR == 2 && col == 0 && tid == 0 && ((wave + 1) % a.wbatch == 0 || wave == a.wcount - 1)) {
+      __threadfence();  // this CTA's colour-0 groups of the batch are stored
+      atomicAdd(a.wdone + wave / a.wbatch, 1u);
     }
   }
   cp_async_wait_all();
@@ -584,7 +598,12 @@ static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
     const int64_t per_wave = grid * Cf::G;
     am.wdone = c->d_wdone;
     am.wcount = (need + grid - 1) / grid;
-    am.wlag = 2 + (per_k > 0 ? (per_k - 1) / per_wave : 0);
+    am.wdep = 1 + (per_k > 0 ? (per_k - 1) / per_wave : 0);
+    am.wbatch = c->merge_batch;
+    // batched arrivals: a wait covers whole batches, so the lead must exceed the dependency by
+    // at least one batch (else a CTA could wait for waves it has not reached itself)
+    const int64_t slack = c->merge_slack > c->merge_batch - 1 ? c->merge_slack : c->merge_batch - 1;
+    am.wlag = am.wdep + 1 + slack;
   }
   TabOff to;
   to.set(N);

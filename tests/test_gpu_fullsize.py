@@ -244,3 +244,41 @@ def test_config5_subbox_matches_oracle():
         del r, rv
     del dc, ctx, u, views
     torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------- merged colour schedule (forced)
+@pytest.mark.parametrize("p", [1, 2, 5, 8, 9, 12, 13, 16])
+@pytest.mark.parametrize("cap,batch,slack", [("0", "4", "4"), ("3", "1", "0"), ("2", "3", "2")])
+def test_merged_colour_schedule_matches_oracle(p, cap, batch, slack, monkeypatch):
+    """Both colour passes in one L2-ordered launch (HDGB_MERGE=1; per-wave arrival counters,
+    colour-1 waves waiting on their colour-0 neighbours) at every staging path, with capped grids
+    and batch/lead settings that make the waits bite: operator applies bitwise equal to the
+    two-launch schedule and within 1e-12 of the oracle, fused PCG (transformed CG mode at p = 2,
+    the merged CG reduction) against the oracle PCG."""
+    from paper_2007_11891_b200.operator import DeviceContext
+
+    n_el, bc, hi, widths = _capped_case(p, False)
+    mesh = hb.Mesh(n_el, (0, 0, 0), hi, bc)
+    octx = O.context(O.basis_1d(p, 0.7), O.Grid(widths, (0, 0, 0), bc), 0.35)
+    u = np.random.default_rng(300 + p).uniform(-1, 1, mesh.n_all(p))
+    ud = _dev(u)
+    monkeypatch.setenv("HDGB_GRID_CAP", cap)
+    monkeypatch.setenv("HDGB_MERGE", "0")
+    ref = [DeviceContext(hb.Basis1D(p, 0.7), mesh, 0.35).apply(ud, v) for v in (0, 1)]
+    monkeypatch.setenv("HDGB_MERGE", "1")
+    monkeypatch.setenv("HDGB_MERGE_BATCH", batch)
+    monkeypatch.setenv("HDGB_MERGE_SLACK", slack)
+    dc = DeviceContext(hb.Basis1D(p, 0.7), mesh, 0.35)
+    for _ in range(2):  # the counters reset at the end of every launch
+        for variant, tr in ((0, False), (1, True)):
+            got = dc.apply(ud, variant)
+            assert torch.equal(got, ref[variant]), variant
+            assert relerr(got.cpu().numpy(), O.apply_op(octx, u, tr)) < TOL
+    F = np.random.default_rng(400 + p).uniform(-1, 1, dc.n_unknown)
+    Fd = dc.unpack(_dev(F))
+    for variant, kind in ((0, 1), (1, 3)):
+        x = torch.zeros_like(Fd)
+        it, rel, conv = dc.pcg(variant, kind, Fd, x, 1e-10, 0.0, 3000)
+        xo, ito, _, convo = _packed_pcg_oracle(octx, kind, F, transformed=bool(variant))
+        assert conv and convo and abs(it - ito) <= 1, (variant, it, ito)
+        assert relerr(dc.pack(x).cpu().numpy(), xo) < 1e-9
