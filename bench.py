@@ -828,36 +828,6 @@ def run_ours(args):
                     "algorithmic_bytes_per_launch": alg_bytes, "plain_apply_frac": cfg2_roof["plain_apply_frac"],
                     "peak_kind": peak_kind}
 
-    # ---- roofline of the dominant kernel: the element-kernel pair (opV colour passes 0 + 1 = one
-    # transformed apply, the core of the plain apply) on an HBM-scale grid, config 3 at p = 8
-    # (44^3, 2.0e7 unknowns, 160 MB per vector >> 126 MB L2), timed above with CUDA events on the
-    # launching stream; 16 B per trace unknown.  Config 2 (8 MB vectors, L2-resident,
-    # 2.3 waves of CTAs) is reported beside it.
-    cfg2_roof = {"workload": "config 2 (16^3, p=8)", "pair_ms": t_tr * 1e3,
-                 "pair_frac": (alg_bytes / t_tr / 1e9) / hbm, "plain_apply_ms": t_k * 1e3,
-                 "plain_apply_frac": (alg_bytes / t_k / 1e9) / hbm,
-                 "traffic": (traffic or {}).get("config2", {}).get("bytes_per_launch")}
-    c3 = large.get("config3_p8")
-    if c3 is not None:
-        N3 = c3["trace_unknowns"]
-        t_pair, t_plain3 = c3["transformed"]["us"] * 1e-6, c3["plain"]["us"] * 1e-6
-        ach = 16 * N3 / t_pair / 1e9
-        roofline = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                    "traffic": (traffic or {}).get("config3_p8", {}).get("bytes_per_launch"),
-                    "kernel": "opV_kernel<9> element kernel pair (colour pass 0 + 1 = one transformed apply)",
-                    "workload": "config 3 at p=8: 44^3 elements, lambda=0, seed 8", "kernel_ms": t_pair * 1e3,
-                    "algorithmic_bytes_per_launch": 16 * N3, "plain_apply_ms": t_plain3 * 1e3,
-                    "plain_apply_frac": 16 * N3 / t_plain3 / 1e9 / hbm, "peak_kind": peak_kind,
-                    "note": "'launch' = both colour passes; 16 B per trace unknown (read u, write r)",
-                    "config2": cfg2_roof}
-    else:
-        roofline = {"bound": "hbm", "achieved": alg_bytes / t_tr / 1e9, "peak": hbm, "unit": "GB/s",
-                    "frac": (alg_bytes / t_tr / 1e9) / hbm, "traffic": cfg2_roof["traffic"],
-                    "kernel": "opV_kernel<9> element kernel pair (colour pass 0 + 1 = one transformed apply)",
-                    "workload": "config 2 (L2-resident: not an HBM-scale point)", "kernel_ms": t_tr * 1e3,
-                    "algorithmic_bytes_per_launch": alg_bytes, "plain_apply_frac": cfg2_roof["plain_apply_frac"],
-                    "peak_kind": peak_kind}
-
     line = {
         "metric": METRIC,
         "value": value, "unit": "trace-DOF/s", "n_gpus": world, "steps": steps, "warmup": warm,
