@@ -173,6 +173,11 @@ int hdgb_halo_add(hdgb_ctx* ctx, double* all, int plane, const double* buf, void
 /* Number of kernels launched by this ctx so far (evidence counter for bench.py). */
 int64_t hdgb_ctx_launches(const hdgb_ctx* ctx);
 
+/* Code paths chosen at create: bit 0 = parity-folded element kernel (B_S[a][1] = sig_a B_S[a][0]
+ * within 2.5e-12, HDGB_EFOLD=0 disables), bit 1 = parity-folded face-kernel products
+ * (N >= 13, HDGB_FOLD=0 disables).  Diagnostics for tests and bench.py. */
+int hdgb_ctx_flags(const hdgb_ctx* ctx);
+
 /* Diagnostics: measured dense DFMA throughput of the current device in TFLOP/s (FP64 roofline
  * denominator for the compute-bound plain operator; MEASURED_PEAKS.json has no FP64 entry). */
 int hdgb_fp64_peak(double* tflops, void* stream);

@@ -74,6 +74,7 @@ SIGNATURES = {
     "hdgb_halo_pack": (ctypes.c_int, [_VP, _VP, ctypes.c_int, _VP, _VP]),
     "hdgb_halo_add": (ctypes.c_int, [_VP, _VP, ctypes.c_int, _VP, _VP]),
     "hdgb_ctx_launches": (_I64, [_VP]),
+    "hdgb_ctx_flags": (ctypes.c_int, [_VP]),
     "hdgb_fp64_peak": (ctypes.c_int, [ctypes.POINTER(_D), _VP]),
 }
 

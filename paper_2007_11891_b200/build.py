@@ -54,6 +54,9 @@ def _compile(src):
 def build(force=False, verbose=False):
     if not force and up_to_date():
         return OUT
+    # the library is stamped with the newest source time seen at the START of the build, so a
+    # source edited while nvcc runs still counts as newer than the library
+    t_src = max(os.path.getmtime(p) for p in _deps())
     os.makedirs(BUILD, exist_ok=True)
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         results = list(ex.map(_compile, _sources()))
@@ -67,6 +70,7 @@ def build(force=False, verbose=False):
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, OUT)
+    os.utime(OUT, (t_src, t_src))
     return OUT
 
 

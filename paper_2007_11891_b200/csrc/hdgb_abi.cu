@@ -54,6 +54,7 @@ int64_t hdgb_ctx_n_all(const hdgb_ctx* c) { return c ? c->n_all : -1; }
 int64_t hdgb_ctx_n_unknown(const hdgb_ctx* c) { return c ? c->n_unknown : -1; }
 int64_t hdgb_ctx_n_faces(const hdgb_ctx* c, int d) { return (c && d >= 0 && d < 3) ? c->g.nf[d] : -1; }
 int64_t hdgb_ctx_launches(const hdgb_ctx* c) { return c ? c->launches : -1; }
+int hdgb_ctx_flags(const hdgb_ctx* c) { return c ? (c->efold ? 1 : 0) | (c->fold_ok ? 2 : 0) : -1; }
 int64_t hdgb_dot_scratch_doubles(void) { return 2 * HDGB_RED_BLOCKS + 8; }
 
 static void free_ctx(hdgb_ctx* c) {
@@ -70,6 +71,8 @@ static void free_ctx(hdgb_ctx* c) {
     if (b) cudaFree(b);
   if (c->d_finfo) cudaFree(c->d_finfo);
   if (c->d_wdone) cudaFree(c->d_wdone);
+  if (c->d_erec) cudaFree(c->d_erec);
+  if (c->d_eal) cudaFree(c->d_eal);
   if (c->d_st) cudaFree(c->d_st);
   if (c->h_st) cudaFreeHost(c->h_st);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
@@ -259,6 +262,9 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
     const int64_t npairs = (int64_t)((g.n1 + 1) / 2) * g.n2 * g.n3;
     CK(cudaMalloc(&c->d_wdone, sizeof(uint32_t) * (npairs + 2)));
     CK(cudaMemset(c->d_wdone, 0, sizeof(uint32_t) * (npairs + 2)));
+    c->npairs = npairs;
+    CK(cudaMalloc(&c->d_erec, sizeof(uint32_t) * 8 * 2 * (npairs > 0 ? npairs : 1)));
+    if (!c->uniform) CK(cudaMalloc(&c->d_eal, sizeof(double) * 4 * 2 * (npairs > 0 ? npairs : 1)));
   }
   CK(cudaMalloc(&c->d_st, sizeof(CGState)));
   CK(cudaMemset(c->d_st, 0, sizeof(CGState)));
@@ -289,8 +295,49 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
     const int nmin = fn ? atoi(fn) : 13;
     c->sig = sig;
     c->fold_ok = ok && !(fe && atoi(fe) == 0) && N >= nmin;
+    // element-kernel folding: B_S[a][1] = sig_a B_S[a][0] (reflection symmetry of the 1D
+    // trace couplings; the reference's eigh-computed S carries up to ~1.3e-12 relative
+    // asymmetry at p = 16, which moves the transformed apply by <= 4e-13 of max|r|)
+    const double* BS = c->h_tab.data() + to.BS;
+    double bmx = 0.0, dev = 0.0;
+    int neven = 0;
+    for (int a = 0; a < N; ++a) {
+      bmx = fmax(bmx, fmax(fabs(BS[2 * a]), fabs(BS[2 * a + 1])));
+      const double sg = (sig >> a & 1u) ? 1.0 : -1.0;
+      dev = fmax(dev, fabs(BS[2 * a + 1] - sg * BS[2 * a]));
+      neven += (sig >> a & 1u) ? 1 : 0;
+    }
+    const char* ef = getenv("HDGB_EFOLD");
+    // default per degree (config-3 sweep, transformed apply at ~2e7 unknowns): folded faster at
+    // p = 3 (160 vs 174 us), 8 (246 vs 252), 12 (275 vs 288), 16 (374 vs 414); slower at p = 2
+    // (296 vs 202) and p = 4 (236 vs 200); HDGB_EFOLD=1 forces it on, =0 off
+    const bool efdef = N == 4 || N >= 6;
+    c->efold = ok && neven == (N + 1) / 2 && dev <= 2.5e-12 * bmx && !(ef && atoi(ef) == 0) &&
+               (efdef || (ef && atoi(ef) == 1));
+    if (c->efold) {
+      int j = 0;
+      for (int a = 0; a < N; ++a)
+        if (sig >> a & 1u) c->perm[j++] = a;
+      for (int a = 0; a < N; ++a)
+        if (!(sig >> a & 1u)) c->perm[j++] = a;
+      std::vector<double> Ss(N * N);  // S' = (S + J S diag(sig)) / 2
+      for (int a = 0; a < N; ++a) {
+        const double sg = (sig >> a & 1u) ? 1.0 : -1.0;
+        c->b0sym[a] = 0.5 * (BS[2 * a] + sg * BS[2 * a + 1]);
+        for (int i = 0; i < N; ++i) Ss[i * N + a] = 0.5 * (S[i * N + a] + sg * S[(N - 1 - i) * N + a]);
+      }
+      const double* w = c->h_tab.data() + to.w;
+      c->h_Tsym.assign(N * N, 0.0);
+      c->h_MSsym.assign(N * N, 0.0);
+      for (int a = 0; a < N; ++a)
+        for (int i = 0; i < N; ++i) {
+          c->h_Tsym[a * N + i] = Ss[i * N + a] * w[i];   // T' = S'^T M
+          c->h_MSsym[i * N + a] = w[i] * Ss[i * N + a];  // MS' = M S'
+        }
+    }
   }
   CK(launch_build_tables(c, c->s));
+  CK(launch_build_erec(c, c->s));
   CK(cudaStreamSynchronize(c->s));
   // validate the preconditioner diagonals on unknown faces (preconditioner.py:89-90, 146-147)
   if (c->uniform) {

@@ -1015,7 +1015,7 @@ cudaError_t launch_plain_post(hdgb_ctx* c, int cg, const double* u, double* r, c
   a.out = r;
   TabOff to;
   to.set(c->N);
-  const double* MS = c->h_tab.data() + to.MS;
+  const double* MS = plain_MS(c);
   const double* w = c->h_tab.data() + to.w;
   switch (c->N) {
 #define HDGB_CASE(n)                                                             \

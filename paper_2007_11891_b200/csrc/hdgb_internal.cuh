@@ -125,6 +125,9 @@ struct OpArgs {
   const double* z;       // CG mode, fused direction update: z (u = p is updated in place via pout)
   double* pout;
   double* xout;          // CG mode, fused direction update: x (deferred x += alpha_prev p_prev)
+  const uint32_t* erec;  // element records [colour][pair][8] (see hdgb_ctx::d_erec)
+  const double* eal;     // non-uniform: alpha0..3 per record
+  int64_t npairs;
   uint32_t* wdone;       // merged colour schedule: per-wave colour-0 arrivals (+ exit ticket)
   int64_t wcount;        //   waves per colour
   int64_t wlag;          //   colour-0 waves ahead of colour-1 wave 0 (placement)
@@ -315,6 +318,15 @@ struct hdgb_ctx {
   // use the parity-folded 1D products (HDGB_FOLD=0 disables)
   uint32_t sig = 0;
   int fold_ok = 0;
+  // element-kernel parity folding (hdgb_op_impl.cuh, MODE bit 4): B_S[a][1] = sig_a B_S[a][0]
+  // to within 2.5e-12 max|B_S| and ceil(N/2) even eigenvectors.  The kernel then runs in a
+  // permuted eigen index (even class first) with the symmetrised B_S column; the plain
+  // operator's face transforms use the symmetrised T = S'^T M and MS = M S' with it, so K is
+  // unchanged to ~1e-14 (HDGB_EFOLD=0 disables)
+  int efold = 0;
+  int perm[HDGB_MAX_N] = {0};       // permuted eigen index j -> a (even class first)
+  double b0sym[HDGB_MAX_N] = {0.0};  // symmetrised B_S[:,0] in natural order
+  std::vector<double> h_Tsym, h_MSsym;
   // L2 working-set target of one z-slab of the colour passes; 0 = one slab.  Slabbing cuts
   // HBM traffic (pass-0 partials stay in L2) but multiplies launches; while the element
   // kernels are issue-bound the single slab is faster (HDGB_SLAB_MB overrides).
@@ -330,6 +342,13 @@ struct hdgb_ctx {
   // faster only at N = 17 (p = 16 460 -> 426 us), so it is the default there; HDGB_MERGE=0/1
   // forces either schedule
   uint32_t* d_wdone = nullptr;
+  // element records of the colour passes (hdgb_op.cu): per colour and element pair index t, the
+  // six face offsets fid * N^2, kinds, shared-face bits and a valid bit (8 words), plus the
+  // metric terms alpha0..3 on non-uniform grids; the element kernel prefetches them with
+  // cp.async three groups ahead instead of computing the geometry on the critical path
+  uint32_t* d_erec = nullptr;
+  double* d_eal = nullptr;
+  int64_t npairs = 0;
   int merge = 1;
   int merge_slack = 4;  // extra colour-0 waves of lead (CTA drift) beyond the neighbour dependency
   int merge_batch = 4;  // colour-0 waves per arrival (one fence + atomic per batch and CTA)
@@ -338,6 +357,17 @@ struct hdgb_ctx {
 namespace hdgb {
 inline int64_t cap_grid(const hdgb_ctx* c, int64_t grid) {
   return (c->grid_cap > 0 && grid > c->grid_cap) ? c->grid_cap : grid;
+}
+// T and MS of the plain operator's face transforms (symmetrised when the element kernel folds)
+inline const double* plain_T(const hdgb_ctx* c) {
+  TabOff to;
+  to.set(c->N);
+  return c->efold ? c->h_Tsym.data() : c->h_tab.data() + to.T;
+}
+inline const double* plain_MS(const hdgb_ctx* c) {
+  TabOff to;
+  to.set(c->N);
+  return c->efold ? c->h_MSsym.data() : c->h_tab.data() + to.MS;
 }
 }  // namespace hdgb
 
@@ -366,6 +396,7 @@ cudaError_t launch_x_final(hdgb_ctx* c, cudaStream_t s);
 cudaError_t launch_diag_user(hdgb_ctx* c, const double* diag, const double* in, double* out, cudaStream_t s);
 int grid_for(int64_t work, int per);
 cudaError_t launch_build_tables(hdgb_ctx* c, cudaStream_t s);
+cudaError_t launch_build_erec(hdgb_ctx* c, cudaStream_t s);
 }  // namespace hdgb
 
 namespace hdgb {

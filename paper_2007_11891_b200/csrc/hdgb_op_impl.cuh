@@ -95,8 +95,9 @@ __device__ __forceinline__ void elem_alpha(const OpArgs& a, const int* c, double
   }
 }
 
-// PU: the colour-0 pass with the fused PCG direction update (MODE bits 0 and 3)
-template <int N, bool PU = false>
+// PU: the colour-0 pass with the fused PCG direction update (MODE bits 0 and 3); FO: the
+// parity-folded kernel (MODE bit 4)
+template <int N, bool PU = false, bool FO = false>
 struct OpVCfg {
   static constexpr int NQ = N * N;                      // threads (face positions) per element
 #ifndef HDGB_OPV_THREADS
@@ -141,7 +142,19 @@ struct OpVCfg {
 #define HDGB_OPV_TMA_NMAX 16
 #endif
   static constexpr bool TMA = N >= HDGB_OPV_TMA_NMIN && N <= HDGB_OPV_TMA_NMAX;
-  static constexpr int FSTR = (TMA && (NQ & 1)) ? NQ + 1 : NQ;  // face slot stride
+  // folded kernel: the even- and odd-class folded faces (sum / difference of the two sides) are
+  // read side by side by lanes of either class; slots FSF doubles apart with FSF mod 16 in
+  // [N, 16 - N] (N <= 8: disjoint banks) or = N (N = 9..15: nearly so) avoid bank conflicts
+  static constexpr int fsf_pad() {
+    if (N >= 16) return 0;
+    for (int p = 0; p < 16; ++p) {
+      const int m = (NQ + p) % 16;
+      if (N <= 8 ? (m >= N && m <= 16 - N) : m == N) return p;
+    }
+    return 0;
+  }
+  static constexpr int FSF = NQ + fsf_pad();
+  static constexpr int FSTR = TMA ? ((NQ & 1) ? NQ + 1 : NQ) : (FO ? FSF : NQ);  // face slot stride
   static constexpr int FS = 6 * FSTR;                   // staged faces of one element
   // U volume of one element: U(a1, a2, a3) at a1 S1 + a2 S2 + a3 S3.  Phase 1 stores (a2, a3)
   // across the lanes, phase 2 reads (a1, a3) (y faces) and (a1, a2) (z faces); the strides are the
@@ -172,23 +185,38 @@ struct OpVCfg {
   __host__ __device__ static constexpr int smem_doubles(bool pupd = false) {
     return pupd ? ZOFF + 4 * G * FS : G * (2 * FS + VS) + (DZS ? N * NQ : 0);
   }
+  // parity-folded kernel (MODE bit 4) with bulk-copy staging: the folded y / z faces go to a
+  // separate buffer (4 NQ per element) after everything else; with cp.async staging they
+  // overwrite the staged faces in place
+  static constexpr int FOFF = (smem_doubles(PU) + 1) / 2 * 2;
+  __host__ __device__ static constexpr int smem_doubles_fold() { return TMA ? FOFF + 4 * G * FSF : smem_doubles(PU); }
+  // colour pass 1 with cp.async staging: the colour-0 partials of the shared faces are staged
+  // with the faces, one group ahead (2 x G x [6][FSTR] after everything else)
+  // (N >= 6: p = 5..11 and 16 2-5 % faster; smaller N lose the occupancy to the extra buffer)
+  static constexpr bool PREV = !TMA && !PU && N >= 6;
+  __host__ __device__ static constexpr int smem_doubles_prev(bool fold) { return (fold ? smem_doubles_fold() : smem_doubles(PU)) + 2 * G * FS; }
+  __host__ __device__ static constexpr int POFF(bool fold) { return fold ? smem_doubles_fold() : smem_doubles(PU); }
 };
 
 // 1D reference-element tables as kernel parameters (constant bank): every compile-time
 // indexed B_S / Lambda entry is a uniform operand, not a load.
+// Folded kernel (MODE bit 4): B0 and Lam are the symmetrised B_S[:,0] and Lambda in the
+// permuted eigen index j (even class first, perm[j] = a), B1 the symmetrised B_S[:,0] in the
+// natural index; sig bit a = eigenvector a even; pS1/pS2/pS3/pN/pNQ[j] = perm[j] times the
+// volume strides / N / N^2 (uniform offsets of the permuted loops).
 template <int N>
 struct OpVConst {
   double B0[N], B1[N], Lam[N];
+  int pS1[N], pS2[N], pS3[N], pN[N], pNQ[N];
+  unsigned sig;
 };
 
-// per element slot, written by one thread per group
-struct ElemInfo {
-  long long fid[6];
-  unsigned off[6];  // fid * N^2: 32-bit element offsets (n_all < 2^32, checked at create)
-  double al[4];
-  int valid;
-  unsigned shared;
-  int kind[6];
+// element record (hdgb_ctx::d_erec, built once per context by build_erec_kernel): face offsets
+// fid * N^2 (32-bit: n_all < 2^32, checked at create), flags (bit 0 valid, bits 1-6 shared
+// faces, bits 8 + 3 s the kind of face s)
+struct __align__(16) ERec {
+  uint32_t off[6];
+  uint32_t flags, spare;
 };
 
 // Merged colour schedule (COLOR = 2): both colour passes in one persistent launch.  Each CTA
@@ -228,14 +256,29 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
 }
 
 // MODE bit 0: CG (Dirichlet rows -> 0, <p, w> and alpha from a fixed-order reduction at the end); bit 1: non-uniform grid (per-element
-// metric terms and dz_inv); bit 2: "g only" (plain core: emit the eigen-space sum of g only).
+// metric terms and dz_inv); bit 2: "g only" (plain core: emit the eigen-space sum of g only);
+// bit 4: parity folding.
+//
+// Parity folding.  The GLL nodes are symmetric, so every 1D eigenvector is even or odd,
+// S[N-1-i][a] = sig_a S[i][a], and so are the trace couplings: B_S[a][1] = sig_a B_S[a][0].
+// The x-line of thread (a2, a3) then needs F = al1 B0[a1] (x0 + sig_a1 x1)
+// + al2 B0[a2] (y0 + sig_a2 y1)[a1, a3] + al3 B0[a3] (z0 + sig_a3 z1)[a1, a2]: ONE folded y and
+// ONE folded z value per point instead of four faces, and every reduction splits into an even
+// and an odd sum, r_lo = E + O, r_hi = E - O (one FMA per point and direction instead of two).
+// The a1 loop of phase 1 and the reductions of phase 2 run in a permuted eigen index j (even
+// class first, perm[j] = a; the even class has ceil(N/2) members), so the class of a loop
+// index is a compile-time fact and perm[j] times a stride is a uniform kernel parameter.  Threads
+// keep their natural face positions; the folded y / z faces overwrite the staged faces in place
+// (bulk-copy staging: separate buffer), in slots N (mod 16) doubles apart so lanes of both
+// classes read them without bank conflicts.
 template <int N, int MODE, int COLOR>
 __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
                                   OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::MINB) opV_kernel(const OpArgs a, int64_t t0, int64_t t1,
                                                           const __grid_constant__ OpVConst<N> K) {
-  using C = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>;
+  using C = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, (MODE & 16) != 0>;
   constexpr int NQ = C::NQ, G = C::G, FS = C::FS, VS = C::VS;
-  constexpr bool UNI = !(MODE & 2), CG = MODE & 1, GONLY = MODE & 4;
+  constexpr bool UNI = !(MODE & 2), CG = MODE & 1, GONLY = MODE & 4, FOLD = MODE & 16;
+  constexpr int NE = (N + 1) / 2;  // FOLD: even-class size (j < NE even)
   // bit 3 (CG, colour 0 only): p = z + beta p (solver.py:320) fused into the staging of this
   // pass: colour 0 updates every face of its elements while staging them and, in a tail loop,
   // the boundary faces whose only element is colour 1; the new p is written back, so colour 1
@@ -258,7 +301,9 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   __shared__ __align__(8) uint64_t sBar[2];  // TMA: one transaction barrier per staging buffer
   double* sF0 = smem;              // 2 x G x [6][FSTR] staged faces
   double* sU = smem + 2 * G * FS;  // G x [N][NQ] volume
-  __shared__ ElemInfo sInfo[2][G];
+  // element records of groups k .. k + 3 (prefetched three groups ahead, slot k % 4)
+  __shared__ ERec sRec[4][G];
+  __shared__ __align__(16) double sAl[4][G][4];  // non-uniform: alpha0..3
   const Geo& g = a.g;
   const int tid = threadIdx.x;
   const int e = tid / NQ, q = tid - (tid / NQ) * NQ;
@@ -268,17 +313,21 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   to.set(N);
   const double gcc0 = a.tab[to.gcc], gcc1 = a.tab[to.gcc + 1];
   // per-thread 1D entries at the thread's own line coordinates
-  const double b0a = a.tab[to.BS + 2 * qa], b1a = a.tab[to.BS + 2 * qa + 1];
-  const double b0b = a.tab[to.BS + 2 * qb], b1b = a.tab[to.BS + 2 * qb + 1];
+  const double b0a = FOLD ? K.B1[qa] : a.tab[to.BS + 2 * qa], b1a = FOLD ? 0.0 : a.tab[to.BS + 2 * qa + 1];
+  const double b0b = FOLD ? K.B1[qb] : a.tab[to.BS + 2 * qb], b1b = FOLD ? 0.0 : a.tab[to.BS + 2 * qb + 1];
   const double lama = a.tab[to.Lam + qa], lamb = a.tab[to.Lam + qb];
   constexpr bool DZR = UNI && !C::DZS;
   double dzr[DZR ? N : 1];
   double* sDz = smem + G * (2 * FS + VS);
   if (DZR) {
 #pragma unroll
-    for (int a1 = 0; a1 < N; ++a1) dzr[DZR ? a1 : 0] = __ldg(a.dz + a1 * NQ + q);  // dz_inv[a1][a2][a3]
+    for (int a1 = 0; a1 < N; ++a1)  // dz_inv[a1][a2][a3] (FOLD: permuted a1)
+      dzr[DZR ? a1 : 0] = __ldg(a.dz + (FOLD ? K.pNQ[a1] : a1 * NQ) + q);
   } else if (UNI) {
-    for (int i = tid; i < N * NQ; i += blockDim.x) sDz[i] = __ldg(a.dz + i);
+    for (int i = tid; i < N * NQ; i += blockDim.x) {
+      const int j1 = i / NQ, t = i - j1 * NQ;
+      sDz[i] = __ldg(a.dz + (FOLD ? K.pNQ[j1] : j1 * NQ) + t);
+    }
   }
 
   const int64_t ngroups = (t1 - t0 + G - 1) / G;
@@ -295,30 +344,28 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       gi = blockIdx.x + k * (int64_t)gridDim.x;
     }
   };
-  auto info = [&](int64_t k, ElemInfo* dst) {
-    if (tid < G) {
-      ElemInfo& I = dst[tid];
+  // record of group k into slot k % 4: 8-byte words, plain (prologue) or cp.async (loop);
+  // groups past the end of this CTA's work get a zero (invalid) record
+  constexpr int RW = UNI ? 4 : 8;  // 8-byte words per element: record (+ alpha0..3)
+  auto fetch = [&](int64_t k, bool async) {
+    const int sl = (int)(k & 3);
+    for (int c = tid; c < G * RW; c += C::NT) {
+      const int ee = c / RW, part = c - ee * RW;
       int col;
       int64_t gi, w;
       slot_item(k, col, gi, w);
-      const int64_t t = t0 + gi * G + tid;
-      Elem E;
-      I.valid = gi < ngroups && t < t1 && pair_elem(g, t, col, E);
-      if (I.valid) {
-        double al[4];
-        elem_alpha(a, E.c, al);
-#pragma unroll
-        for (int s = 0; s < 6; ++s) {
-          I.fid[s] = E.fid[s];
-          I.off[s] = (unsigned)E.fid[s] * (unsigned)NQ;
-          I.kind[s] = face_kind(g, s >> 1, E.c[s >> 1] + (s & 1));
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) I.al[k] = al[k];
-        I.shared = E.shared;
-      }
+      const int64_t t = t0 + gi * G + ee;
+      const bool ok = k < nslots && gi < ngroups && t < t1;
+      const int64_t ri = (int64_t)col * a.npairs + t;
+      double* dst = part < 4 ? reinterpret_cast<double*>(&sRec[sl][ee]) + part : &sAl[sl][ee][part - 4];
+      const double* src = part < 4 ? reinterpret_cast<const double*>(a.erec + 8 * ri) + part : a.eal + 4 * ri + (part - 4);
+      if (!ok) *dst = 0.0;
+      else if (async) cp_async8(dst, src);
+      else *dst = __ldg(src);
     }
   };
+  constexpr bool PREV = C::PREV && COLOR == 1;  // colour-0 partials staged with the faces
+  double* sP0 = smem + C::POFF(FOLD);            // PREV: 2 x G x [6][FSTR] staged partials
   double* sZ0 = smem + C::ZOFF;      // PUPD: 2 x G x [6][FSTR] staged z
   double* sX0 = sZ0 + 2 * G * FS;    // PUPD: 2 x G x [6][FSTR] staged x
   if (TMA && tid == 0) {
@@ -335,14 +382,14 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   // vector may end there).  The lanes' plain stores are ordered before the arrive by the
   // warp barrier; the arrive's transaction count is the warp's sum of copied bytes (a
   // complete_tx may land before the expect_tx: the count is allowed to go negative).
-  auto stage_tma = [&](const ElemInfo* inf, double* buf, int bi) {
+  auto stage_tma = [&](const ERec* inf, double* buf, int bi) {
     if (tid >= 32) return;
     constexpr int NC = PUPD ? 18 : 6;
     fence_proxy_async();  // the buffer's previous generic accesses (closing barrier) before the refill
     uint32_t bytes = 0;
     for (int c = tid; c < G * NC; c += 32) {
       const int ee = c / NC, k = c - ee * NC, sface = k % 6;
-      if (!inf[ee].valid) continue;
+      if (!(inf[ee].flags & 1u)) continue;
       const unsigned off = inf[ee].off[sface];
       const double* src = k < 6 ? a.u : (k < 12 ? a.z : a.xout);
       double* dst = (k < 6 ? buf : (k < 12 ? sZ0 : sX0) + bi * G * FS) + ee * FS + sface * FSTR;
@@ -364,41 +411,53 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     __syncwarp();
     if (tid == 0) mbar_expect_tx(&sBar[bi], bytes);
   };
-  auto stage = [&](const ElemInfo* inf, double* buf, int bi) {
+  auto stage = [&](const ERec* inf, double* buf, int bi) {
     if (TMA) {
       stage_tma(inf, buf, bi);
       return;
     }
-    if (act && inf[e].valid) {
+    if (act && (inf[e].flags & 1u)) {
       double* dst = buf + e * FS + q;
 #pragma unroll
-      for (int s = 0; s < 6; ++s) cp_async8(dst + s * NQ, a.u + (inf[e].off[s] + (unsigned)q));
+      for (int s = 0; s < 6; ++s) cp_async8(dst + s * FSTR, a.u + (inf[e].off[s] + (unsigned)q));
+      if (PREV) {
+        const uint32_t sh = inf[e].flags >> 1;
+        double* dp = sP0 + bi * G * FS + e * FS + q;
+#pragma unroll
+        for (int s = 0; s < 6; ++s)
+          if (sh >> s & 1u) cp_async8(dp + s * FSTR, a.r + (inf[e].off[s] + (unsigned)q));
+      }
       if (PUPD) {
         double* dz = sZ0 + bi * G * FS + e * FS + q;
         double* dx = sX0 + bi * G * FS + e * FS + q;
 #pragma unroll
-        for (int s = 0; s < 6; ++s) cp_async8(dz + s * NQ, a.z + (inf[e].off[s] + (unsigned)q));
+        for (int s = 0; s < 6; ++s) cp_async8(dz + s * FSTR, a.z + (inf[e].off[s] + (unsigned)q));
 #pragma unroll
-        for (int s = 0; s < 6; ++s) cp_async8(dx + s * NQ, a.xout + (inf[e].off[s] + (unsigned)q));
+        for (int s = 0; s < 6; ++s) cp_async8(dx + s * FSTR, a.xout + (inf[e].off[s] + (unsigned)q));
       }
     }
   };
 
   double dacc = 0.0;  // CG: this thread's share of <p, w> (fixed grid -> reproducible)
   int64_t verified = -1;  // merged schedule: colour-0 waves known complete (thread 0)
-  if (nslots > 0) info(0, sInfo[0]);
+  // records of groups 0..2 now; group k + 3's is fetched with the faces of group k + 1, so it
+  // has landed (wait_group of iteration k + 1) and been published (its next barrier) before the
+  // faces of group k + 3 are staged in iteration k + 2
+  fetch(0, false);
+  fetch(1, false);
+  fetch(2, false);
   __syncthreads();
   if (!CG) pdl_wait();  // u and r come from earlier kernels
-  if (nslots > 0) stage(sInfo[0], sF0, 0);
+  if (nslots > 0) stage(sRec[0], sF0, 0);
   cp_async_commit();
   for (int64_t k = 0; k < nslots; ++k) {
     const int buf = (int)(k & 1);
-    if (k + 1 < nslots) info(k + 1, sInfo[buf ^ 1]);
     __syncthreads();
-    if (k + 1 < nslots) stage(sInfo[buf ^ 1], sF0 + (buf ^ 1) * G * FS, buf ^ 1);
+    if (k + 1 < nslots) stage(sRec[(k + 1) & 3], sF0 + (buf ^ 1) * G * FS, buf ^ 1);
+    if (k + 3 < nslots) fetch(k + 3, true);
     cp_async_commit();
+    asm volatile("cp.async.wait_group 1;\n" ::);
     if (TMA) mbar_wait(&sBar[buf], (uint32_t)(k >> 1) & 1u);
-    else asm volatile("cp.async.wait_group 1;\n" ::);
     int col;
     int64_t gi_unused, wave;
     slot_item(k, col, gi_unused, wave);
@@ -409,43 +468,71 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
         }
       verified = need > verified ? need : verified;
     }
-    // element geometry into registers once (sInfo[buf] was published a barrier ago)
-    const ElemInfo& I = sInfo[buf][act ? e : 0];
-    const bool on = act && I.valid;
+    // element geometry into registers once (record k was published two barriers ago)
+    const ERec& I = sRec[k & 3][act ? e : 0];
+    const uint32_t flags = I.flags;
+    const bool on = act && (flags & 1u);
     unsigned off[6];
     int kinds[6];
 #pragma unroll
     for (int s2 = 0; s2 < 6; ++s2) {
       off[s2] = I.off[s2] + (unsigned)q;
-      kinds[s2] = CG ? I.kind[s2] : 0;
+      kinds[s2] = CG ? (int)(flags >> (8 + 3 * s2) & 7u) : 0;
     }
-    const unsigned shared = I.shared;
-    const double al0 = I.al[0], al1 = I.al[1], al2 = I.al[2], al3 = I.al[3];
+    const unsigned shared = flags >> 1 & 63u;
+    const double* alp = UNI ? a.al_u : sAl[k & 3][act ? e : 0];
+    const double al0 = alp[0], al1 = alp[1], al2 = alp[2], al3 = alp[3];
     double* sFw = sF0 + buf * G * FS + (act ? e : 0) * FS;
     double* fb[6];  // face s of the element: fb[s][position]
 #pragma unroll
     for (int s2 = 0; s2 < 6; ++s2) fb[s2] = sFw + s2 * FSTR + ((TMA && (NQ & 1)) ? (I.off[s2] & 1u) : 0u);
     double* vU = sU + (act ? e : 0) * VS;
+    const int own = q;  // this thread's face position
     if (PUPD && on) {  // position q of every face is this thread's own copy (cp.async) or
                        // complete for every thread (TMA barrier): no extra CTA barrier needed
       const double* sZ = sZ0 + buf * G * FS + (act ? e : 0) * FS;
       const double* sX = sX0 + buf * G * FS + (act ? e : 0) * FS;
 #pragma unroll
       for (int s = 0; s < 6; ++s) {
-        double* fp = fb[s] + q;
-        const int64_t so = (fb[s] - sFw) + q;
+        double* fp = fb[s] + own;
+        const int64_t so = (fb[s] - sFw) + own;
         const double po = *fp, pn = fma(beta, po, sZ[so]);
         *fp = pn;
         a.pout[off[s]] = pn;
         a.xout[off[s]] = fma(alpha_prev, po, sX[so]);
       }
     }
+    // FOLD: raw own values (self terms, <p, w>) into registers, folded y / z faces out
+    double rw[6];
+    // folded faces in permuted order: y (sum / difference of the two sides) [j1][j3], z [j1][j2];
+    // phase 1 reads the class of its own a2 (y) and a3 (z)
+    const double* ysel = nullptr;
+    const double* zsel = nullptr;
+    if (FOLD) {
+      double* fo = TMA ? smem + C::FOFF + (act ? e : 0) * 4 * C::FSF : nullptr;
+      double* ys = TMA ? fo : fb[2];
+      double* yd = TMA ? fo + C::FSF : fb[3];
+      double* zs = TMA ? fo + 2 * C::FSF : fb[4];
+      double* zd = TMA ? fo + 3 * C::FSF : fb[5];
+      if (on) {
+#pragma unroll
+        for (int s = 0; s < 6; ++s) rw[s] = fb[s][own];
+        ys[q] = rw[2] + rw[3];
+        yd[q] = rw[2] - rw[3];
+        zs[q] = rw[4] + rw[5];
+        zd[q] = rw[4] - rw[5];
+      }
+      ysel = (K.sig >> qa & 1u) ? ys : yd;  // class of a2 = qa
+      zsel = (K.sig >> qb & 1u) ? zs : zd;  // class of a3 = qb
+    }
     __syncthreads();  // staged faces (and their update) visible to the whole CTA
     // colour-0 partials of the shared faces at q: issued now, consumed at the emits
     double prev[6];
     if (col == 1 && on) {
+      const double* sP = sP0 + buf * G * FS + (act ? e : 0) * FS + q;
 #pragma unroll
-      for (int s = 0; s < 6; ++s) prev[s] = (shared >> s & 1u) ? __ldcg(a.r + off[s]) : 0.0;
+      for (int s = 0; s < 6; ++s)
+        prev[s] = (shared >> s & 1u) ? (PREV ? sP[s * FSTR] : __ldcg(a.r + off[s])) : 0.0;
     }
     // contribution alpha_d GCC_ll u - g (operator.py:243-257) at position q of face s;
     // ua = alpha_d u, ur = u
@@ -459,7 +546,28 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       }
       a.r[off[s]] = val;
     };
-    if (on) {  // phase 1: x-line of (a2, a3) = (qa, qb)
+    if (FOLD && on) {  // phase 1, folded: x-line of (a2, a3) = (qa, qb), a1 = perm[j] in class order
+      const double x0 = al1 * rw[0], x1 = al1 * rw[1];
+      const double xs = x0 + x1, xd = x0 - x1;
+      const double by = al2 * b0a, bz = al3 * b0b;
+      const double base = UNI ? 0.0 : a.lam * al0 + al2 * lama + al3 * lamb;
+      double ex = 0.0, ox = 0.0;
+#pragma unroll
+      for (int a1 = 0; a1 < N; ++a1) {
+        double F = K.B0[a1] * (a1 < NE ? xs : xd);
+        F = fma(by, ysel[K.pN[a1] + qb], F);
+        F = fma(bz, zsel[K.pN[a1] + qa], F);
+        const double dzv = DZR ? dzr[DZR ? a1 : 0]
+                               : (UNI ? sDz[a1 * NQ + q] : __drcp_rn(fma(al1, K.Lam[a1], base)));  // EigenScale3D
+        const double U = F * dzv;
+        vU[K.pS1[a1] + qa * C::S2 + qb * C::S3] = U;
+        if (a1 < NE) ex = fma(K.B0[a1], U, ex);
+        else ox = fma(K.B0[a1], U, ox);
+      }
+      emit(0, al1 * (ex + ox), x0, rw[0]);
+      emit(1, al1 * (ex - ox), x1, rw[1]);
+    }
+    if (!FOLD && on) {  // phase 1: x-line of (a2, a3) = (qa, qb)
       const double xr0 = fb[0][q], xr1 = fb[1][q];
       const double x0 = al1 * xr0, x1 = al1 * xr1;
       const double by0 = al2 * b0a, by1 = al2 * b1a, bz0 = al3 * b0b, bz1 = al3 * b1b;
@@ -490,21 +598,44 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       const double* ycol = vU + qa * C::S1 + qb * C::S3;  // over a2
       const double* zrow = vU + qa * C::S1 + qb * C::S2;  // over a3
       double ay0 = 0.0, ay1 = 0.0, az0 = 0.0, az1 = 0.0;
+      if (FOLD) {  // even (E) and odd (O) sums: r_lo = E + O, r_hi = E - O
 #pragma unroll
-      for (int k = 0; k < N; ++k) {
-        const double vy = ycol[k * C::S2], vz = zrow[k * C::S3];
-        ay0 = fma(K.B0[k], vy, ay0);
-        ay1 = fma(K.B1[k], vy, ay1);
-        az0 = fma(K.B0[k], vz, az0);
-        az1 = fma(K.B1[k], vz, az1);
+        for (int k = 0; k < N; ++k) {
+          const double vy = ycol[K.pS2[k]], vz = zrow[K.pS3[k]];
+          if (k < NE) {
+            ay0 = fma(K.B0[k], vy, ay0);
+            az0 = fma(K.B0[k], vz, az0);
+          } else {
+            ay1 = fma(K.B0[k], vy, ay1);
+            az1 = fma(K.B0[k], vz, az1);
+          }
+        }
+        const double ey = ay0, ez = az0;
+        ay0 = ey + ay1;
+        ay1 = ey - ay1;
+        az0 = ez + az1;
+        az1 = ez - az1;
+      } else {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const double vy = ycol[k * C::S2], vz = zrow[k * C::S3];
+          ay0 = fma(K.B0[k], vy, ay0);
+          ay1 = fma(K.B1[k], vy, ay1);
+          az0 = fma(K.B0[k], vz, az0);
+          az1 = fma(K.B1[k], vz, az1);
+        }
       }
-      const double yr0 = fb[2][q], yr1 = fb[3][q], zr0 = fb[4][q], zr1 = fb[5][q];
+      const double yr0 = FOLD ? rw[2] : fb[2][q], yr1 = FOLD ? rw[3] : fb[3][q];
+      const double zr0 = FOLD ? rw[4] : fb[4][q], zr1 = FOLD ? rw[5] : fb[5][q];
       emit(2, al2 * ay0, al2 * yr0, yr0);
       emit(3, al2 * ay1, al2 * yr1, yr1);
       emit(4, al3 * az0, al3 * zr0, zr0);
       emit(5, al3 * az1, al3 * zr1, zr1);
     }
-    __syncthreads();  // staging buffer, volume and element info are reused
+    // the staging buffer and volume of this group are reused by the next groups behind the next
+    // iteration's first barrier (its record slot three groups later); only the merged
+    // schedule's arrival counter needs every thread's stores of this group done here
+    if (COLOR == 2) __syncthreads();
     if (COLOR == 2 && col == 0 && tid == 0 && ((wave + 1) % a.wbatch == 0 || wave == a.wcount - 1)) {
       __threadfence();  // this CTA's colour-0 groups of the batch are stored
       atomicAdd(a.wdone + wave / a.wbatch, 1u);
@@ -579,10 +710,15 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
 
 template <int N, int MODE, int COLOR>
 static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_t t1, cudaStream_t s) {
-  using Cf = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>;
-  static_assert(sizeof(double) * Cf::smem_doubles((MODE & 9) == 9 && COLOR == 0) <= 227 * 1024,
-                "element kernel shared memory exceeds 227 KB");
-  const size_t smem = sizeof(double) * (size_t)Cf::smem_doubles((MODE & 9) == 9 && COLOR == 0);
+  constexpr bool FOLD = MODE & 16;
+  if constexpr (!FOLD) {
+    if (c->efold) return launch_passV<N, MODE | 16, COLOR>(c, a, t0, t1, s);
+  }
+  using Cf = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, FOLD>;
+  constexpr int SMD = (Cf::PREV && COLOR == 1) ? Cf::smem_doubles_prev(FOLD)
+                     : (FOLD ? Cf::smem_doubles_fold() : Cf::smem_doubles((MODE & 9) == 9 && COLOR == 0));
+  static_assert(sizeof(double) * SMD <= 227 * 1024, "element kernel shared memory exceeds 227 KB");
+  const size_t smem = sizeof(double) * (size_t)SMD;
   auto kern = opV_kernel<N, MODE, COLOR>;
   static int cache[16] = {0};
   int64_t grid = 0;
@@ -609,10 +745,17 @@ static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
   to.set(N);
   OpVConst<N> K;
   for (int q = 0; q < N; ++q) {
-    K.B0[q] = c->h_tab[to.BS + 2 * q];
-    K.B1[q] = c->h_tab[to.BS + 2 * q + 1];
-    K.Lam[q] = c->h_tab[to.Lam + q];
+    const int aq = FOLD ? c->perm[q] : q;
+    K.B0[q] = FOLD ? c->b0sym[aq] : c->h_tab[to.BS + 2 * q];
+    K.B1[q] = FOLD ? c->b0sym[q] : c->h_tab[to.BS + 2 * q + 1];
+    K.Lam[q] = c->h_tab[to.Lam + aq];
+    K.pS1[q] = aq * Cf::S1;
+    K.pS2[q] = aq * Cf::S2;
+    K.pS3[q] = aq * Cf::S3;
+    K.pN[q] = aq * N;
+    K.pNQ[q] = aq * N * N;
   }
+  K.sig = c->sig;
   cudaError_t le = launch_pdl(kern, dim3((unsigned)grid), dim3(Cf::NT), smem, s, am, t0, t1, K);
   c->launches++;
   return le;
@@ -636,12 +779,9 @@ static cudaError_t launch_t(hdgb_ctx* c, const double* u, double* r, cudaStream_
   const Geo& g = c->g;
   if (g.ne == 0) return cudaSuccess;
   if (PLAIN) {
-    TabOff to;
-    to.set(N);
     cudaError_t e = (MODE & 1) && c->pupd_z
-                        ? launch_face_transform_pupd(c, c->h_tab.data() + to.T, c->pupd_z, const_cast<double*>(u),
-                                                     c->d_hat, s)
-                        : launch_face_transform(c, c->h_tab.data() + to.T, u, c->d_hat, s, 1);
+                        ? launch_face_transform_pupd(c, plain_T(c), c->pupd_z, const_cast<double*>(u), c->d_hat, s)
+                        : launch_face_transform(c, plain_T(c), u, c->d_hat, s, 1);
     if (e != cudaSuccess) return e;
     a.u = c->d_hat;
   }
@@ -653,6 +793,9 @@ static cudaError_t launch_t(hdgb_ctx* c, const double* u, double* r, cudaStream_
   a.uniform = c->uniform;
   a.st = c->d_st;
   a.part = c->d_part;
+  a.erec = c->d_erec;
+  a.eal = c->d_eal;
+  a.npairs = c->npairs;
   // z-slabs of element pairs, sized so two slabs of face data stay L2-resident
   const int64_t hp = (g.n1 + 1) / 2;
   const int64_t per_k = hp * g.n2;  // pairs per z-layer

@@ -219,6 +219,11 @@ class DeviceContext:
     def launches(self):
         return int(_lib.lib().hdgb_ctx_launches(self.handle))
 
+    @property
+    def flags(self):
+        """Code paths chosen at create (hdgb_ctx_flags): bit 0 folded element kernel, bit 1 folded face products."""
+        return int(_lib.lib().hdgb_ctx_flags(self.handle))
+
     # -- entry points
     def apply(self, u, variant, out=None):
         r = self.empty() if out is None else out

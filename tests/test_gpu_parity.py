@@ -487,3 +487,26 @@ def test_parity_folded_face_products(p, fold, monkeypatch):
                           np.zeros_like(Fp))
     assert conv and abs(it - ito) <= 1, (it, ito)
     assert relerr(dc.pack(x).cpu().numpy(), xo) < 1e-9
+
+
+@pytest.mark.parametrize("p", list(range(1, 17)))
+def test_folded_element_kernel_matches_oracle(p, monkeypatch):
+    """Parity-folded element kernel (default, hdgb_ctx_flags bit 0) and the unfolded fallback
+    (HDGB_EFOLD=0) against the oracle at every degree, with a capped grid so every CTA walks
+    several element groups: transformed apply (symmetrised B_S: <= ~4e-13 from the reference
+    basis), plain apply (symmetrised T / MS with it: K unchanged to ~1e-14)."""
+    bc = ("neumann", "dirichlet", "dirichlet", "neumann", "neumann", "dirichlet")
+    n_el, hi = (4, 3, 3), (1.5, 1.0, 1.0)
+    mesh = hb.Mesh(n_el, (0, 0, 0), hi, bc)
+    tau = 0.039 if p % 2 else 0.78125
+    octx = O.context(O.basis_1d(p, tau), O.Grid.uniform(n_el, (0, 0, 0), hi, bc), 0.3)
+    u = np.random.default_rng(100 + p).uniform(-1, 1, mesh.n_all(p))
+    ref = {tr: O.apply_op(octx, u, tr) for tr in (False, True)}
+    monkeypatch.setenv("HDGB_GRID_CAP", "2")
+    for efold in ("1", "0"):
+        monkeypatch.setenv("HDGB_EFOLD", efold)
+        dc = hb.DeviceContext(hb.Basis1D(p, tau), mesh, 0.3)
+        assert (dc.flags & 1) == (1 if efold == "1" else 0)
+        for variant, tr in ((0, False), (1, True)):
+            assert relerr(dc.apply(_dev(u), variant).cpu().numpy(), ref[tr]) < TOL, (efold, variant)
+        del dc
