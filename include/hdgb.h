@@ -36,7 +36,7 @@ typedef enum {
   HDGB_EINVAL = 1,      /* -> ValueError (shapes, arguments, config)                   */
   HDGB_EBREAKDOWN = 2,  /* -> FloatingPointError (CG curvature <= 0 / non-finite)     */
   HDGB_ECUDA = 3,       /* -> RuntimeError (CUDA runtime failure)                      */
-  HDGB_ENCCL = 4,       /* -> RuntimeError (collective failure; reserved)              */
+  HDGB_ENCCL = 4,       /* -> RuntimeError (NCCL missing or a collective failed)       */
   HDGB_ENONFINITE = 5   /* -> FloatingPointError (non-finite residual)                 */
 } hdgb_status;
 
@@ -169,6 +169,31 @@ int hdgb_vec_axpby(int64_t n, double a, const double* x, double b, const double*
  * buffer back into the plane. */
 int hdgb_halo_pack(hdgb_ctx* ctx, const double* all, int plane, double* buf, void* stream);
 int hdgb_halo_add(hdgb_ctx* ctx, double* all, int plane, const double* buf, void* stream);
+
+/* ---- x-slab groups (no counterpart in the single-process reference: solver.py:282-321
+ * and hdg_op_3d (operator.py:261-267) over a grid split along x).  A process holds `nlocal`
+ * consecutive slabs [first_slab, first_slab + nlocal) of a job of `nslabs` slabs, one ctx each
+ * (same device, degree and n2 x n3 cross-section; interface sides HALO_PEER low / HALO_OWNED high,
+ * see distributed.slab_side_kinds), and is rank `proc` of `nprocs` processes holding consecutive
+ * slab ranges.  Neighbouring slabs in the process exchange interface planes in device memory,
+ * across processes over NCCL (libnccl.so.2 loaded at run time; HDGB_NCCL_LIB overrides the path):
+ * all processes pass the same 128-byte id from hdgb_nccl_unique_id (process 0 makes it, the
+ * caller broadcasts it); nccl_id may be NULL only when nprocs == 1.  Destroy the group before
+ * its contexts.  Array arguments hold one device vector per local slab. */
+typedef struct hdgb_slab_group hdgb_slab_group;
+int hdgb_nccl_unique_id(void* id_out /* 128 bytes */);
+int hdgb_slab_group_create(hdgb_ctx* const* ctxs, int nlocal, int first_slab, int nslabs, int proc, int nprocs,
+                           const void* nccl_id, hdgb_slab_group** out);
+int hdgb_slab_group_destroy(hdgb_slab_group* group);
+/* r = K u on every slab, interface planes exchanged (both copies hold the full residual). */
+int hdgb_slab_apply(hdgb_slab_group* group, int variant, const double* const* u, double* const* r, void* stream);
+/* Fused PCG over the group: per iteration one interface exchange of w and two reductions (local
+ * fixed-order sums + ncclAllReduce), the rest as in hdgb_pcg; iterations run as CUDA graphs of 8
+ * and the host reads the done flag of one batch while the next runs.  x is in/out per slab; the
+ * interface copies of x agree bitwise. */
+int hdgb_slab_pcg(hdgb_slab_group* group, int variant, int prec, const double* const* F, double* const* x,
+                  double rtol, double atol, int32_t max_iters, int32_t* iters, double* relres, int32_t* converged,
+                  void* stream);
 
 /* Number of kernels launched by this ctx so far (evidence counter for bench.py). */
 int64_t hdgb_ctx_launches(const hdgb_ctx* ctx);

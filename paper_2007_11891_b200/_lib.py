@@ -76,6 +76,13 @@ SIGNATURES = {
     "hdgb_ctx_launches": (_I64, [_VP]),
     "hdgb_ctx_flags": (ctypes.c_int, [_VP]),
     "hdgb_fp64_peak": (ctypes.c_int, [ctypes.POINTER(_D), _VP]),
+    "hdgb_nccl_unique_id": (ctypes.c_int, [_VP]),
+    "hdgb_slab_group_create": (ctypes.c_int, [ctypes.POINTER(_VP), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                              ctypes.c_int, _VP, ctypes.POINTER(_VP)]),
+    "hdgb_slab_group_destroy": (ctypes.c_int, [_VP]),
+    "hdgb_slab_apply": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.POINTER(_VP), ctypes.POINTER(_VP), _VP]),
+    "hdgb_slab_pcg": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_VP), ctypes.POINTER(_VP), _D, _D,
+                                     _I32, ctypes.POINTER(_I32), ctypes.POINTER(_D), ctypes.POINTER(_I32), _VP]),
 }
 
 _lib = None

@@ -38,7 +38,6 @@ static int einval(const std::string& m) {
   g_err = m;
   return HDGB_EINVAL;
 }
-enum { V_X = 0, V_R = 1, V_Z = 2, V_P = 3, V_W = 4, V_F = 5 };
 // the face-block kernels stream vectors with 16-byte bulk copies
 static bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 }  // namespace hdgb
@@ -618,6 +617,34 @@ int hdgb_vec_axpby(int64_t n, double a, const double* x, double b, const double*
 #ifndef HDGB_PUPD_NMAX
 #define HDGB_PUPD_NMAX 16
 #endif
+}  // extern "C"
+
+namespace hdgb {
+// First half of an iteration: the direction update fused into the operator and w = K p with
+// <p, w> (and, single-context, alpha); leaves pupd_x set for the second half.
+cudaError_t enqueue_op_half(hdgb_ctx* c, int variant, cudaStream_t s) {
+  double* v = c->d_vec;
+  cudaError_t e;
+  c->pupd_z = v + V_Z * c->vstride;
+  if (variant == HDGB_TRANSFORMED && (c->N < HDGB_PUPD_NMIN || c->N > HDGB_PUPD_NMAX)) {
+    if ((e = launch_p_update(c, s)) != cudaSuccess) return e;  // p and the deferred x
+    c->pupd_z = nullptr;
+  }
+  c->pupd_x = v + V_X * c->vstride;
+  e = launch_op(c, variant, MODE_CG, v + V_P * c->vstride, v + V_W * c->vstride, s);
+  c->pupd_z = nullptr;
+  return e;
+}
+// Second half: x, r update, z = P r, ||r||, <r, z> (and, single-context, the decisions).
+cudaError_t enqueue_update_half(hdgb_ctx* c, int prec, cudaStream_t s, cudaGraphConditionalHandle h, int has_loop) {
+  cudaError_t e = launch_cg_update(c, prec, s, h, has_loop);
+  c->pupd_x = nullptr;
+  return e;
+}
+}  // namespace hdgb
+
+extern "C" {
+
 static cudaError_t enqueue_iteration(hdgb_ctx* c, int variant, int prec, cudaGraphConditionalHandle h, int has_loop) {
   double* v = c->d_vec;
   cudaError_t e;

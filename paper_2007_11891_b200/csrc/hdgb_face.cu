@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
   }
   const double beta = PUPD ? a.st->beta : 0.0;
   const double alpha = (XUPD || RUPD) ? a.st->alpha : 0.0;
+  const bool pwall = (POST && CG) ? a.st->dist != 0 : false;  // slab-group <p, w> (kind_counts_pw)
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t sBar[C::NG][S];
   __shared__ double sWq[N];  // FX_POST: quadrature weights (dynamic index: keep out of the constant bank)
@@ -570,7 +571,7 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
         if (CG) {  // final w: Dirichlet row -> 0, <p, w> (p = u here)
           const int kind = finfo_kind(__ldg(finfo + f0 + fi));
           if (kind == HDGB_DIRICHLET) v = 0.0;
-          if (kind_counts(kind)) rz = fma(u0, v, rz);
+          if (kind_counts_pw(kind, pwall)) rz = fma(u0, v, rz);
         }
       }
       a.out[gi] = v;
@@ -1137,7 +1138,6 @@ cudaError_t launch_expand_table(hdgb_ctx* c, int kind, double* out, cudaStream_t
 }
 
 // CG vector slots inside c->d_vec
-enum { V_X = 0, V_R = 1, V_Z = 2, V_P = 3, V_W = 4, V_F = 5 };
 
 cudaError_t launch_cg_init(hdgb_ctx* c, int kind, cudaStream_t s) {
   FaceArgs a = base_args(c, kind);

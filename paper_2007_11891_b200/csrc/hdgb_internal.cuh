@@ -21,6 +21,7 @@
 namespace hdgb {
 
 enum { MODE_APPLY = 0, MODE_CG = 1 };
+enum { V_X = 0, V_R = 1, V_Z = 2, V_P = 3, V_W = 4, V_F = 5 };  // PCG vectors in hdgb_ctx::d_vec
 
 // Mesh geometry in closed form (replaces the int64 index arrays of mesh.py:105-137).
 struct Geo {
@@ -73,6 +74,9 @@ __host__ __device__ inline int face_class(const Geo& g, int d, int plane) {
 }
 __host__ __device__ inline bool kind_unknown(int k) { return k != HDGB_DIRICHLET; }
 __host__ __device__ inline bool kind_counts(int k) { return k != HDGB_DIRICHLET && k != HDGB_HALO_PEER; }
+// <p, w> of a slab solve is taken on the rank-local partial w, before the interface exchange:
+// both copies of an interface face count (their partials sum to the full w)
+__host__ __device__ inline bool kind_counts_pw(int k, bool dist) { return dist ? k != HDGB_DIRICHLET : kind_counts(k); }
 
 // Small constant tables, one contiguous device block (offsets in doubles).
 struct TabOff {
@@ -94,7 +98,9 @@ struct TabOff {
 struct CGState {
   double rho, alpha, beta, norm0, thr, rn, pw, rr, rz, relres, rtol, atol;
   double pw0;       // colour-0 part of <p, w> (transformed operator)
-  int32_t it, max_iters, done, status, converged, pad;
+  // dist: slab-group solve (hdgb_slab.cu): the kernels only publish their rank-local sums
+  // (pw, rr, rz) and the group's decide kernel runs the recurrences on the global sums
+  int32_t it, max_iters, done, status, converged, dist;
   uint32_t cnt[8];  // last-CTA tickets of the reduction kernels
 };
 
@@ -102,6 +108,7 @@ struct CGState {
 // last CTA of the kernel that finishes the operator
 __device__ __forceinline__ void cg_set_alpha(CGState* st, double pw) {
   st->pw = pw;
+  if (st->dist) return;
   if (!isfinite(pw) || pw <= 0.0) {
     st->status = HDGB_EBREAKDOWN;
     st->done = 1;
@@ -216,8 +223,9 @@ __device__ __forceinline__ void final_sum2(const double* part, int nb, double& a
 
 // PCG scalar recurrences (solver.py:290-321), run by thread 0 of the last CTA.
 __device__ __forceinline__ void cg_init_r(CGState* st, double rr) {  // r0 = F - K x0
-  const double rn = sqrt(rr);
   st->rr = rr;
+  if (st->dist) return;
+  const double rn = sqrt(rr);
   st->norm0 = rn;
   st->rn = rn;
   st->it = 0;
@@ -235,14 +243,16 @@ __device__ __forceinline__ void cg_init_r(CGState* st, double rr) {  // r0 = F -
 }
 // beta = 0 before the first iteration: the fused direction update (plain PCG) then gives p = z
 __device__ __forceinline__ void cg_init_z(CGState* st, double rz) {
-  st->rho = rz;
   st->rz = rz;
+  if (st->dist) return;
+  st->rho = rz;
   st->beta = 0.0;
   st->alpha = 0.0;  // the deferred x update of the first iteration adds 0 * p
 }
 __device__ __forceinline__ void cg_update_r(CGState* st, double rr) {  // after x += a p, r -= a w
-  const double rn = sqrt(rr);
   st->rr = rr;
+  if (st->dist) return;
+  const double rn = sqrt(rr);
   st->it += 1;
   st->rn = rn;
   if (!isfinite(rn)) {
@@ -259,6 +269,7 @@ __device__ __forceinline__ void cg_update_r(CGState* st, double rr) {  // after 
 }
 __device__ __forceinline__ void cg_update_z(CGState* st, double rz) {  // beta = rho'/rho
   st->rz = rz;
+  if (st->dist) return;
   st->beta = rz / st->rho;
   st->rho = rz;
 }
@@ -397,6 +408,10 @@ cudaError_t launch_diag_user(hdgb_ctx* c, const double* diag, const double* in, 
 int grid_for(int64_t work, int per);
 cudaError_t launch_build_tables(hdgb_ctx* c, cudaStream_t s);
 cudaError_t launch_build_erec(hdgb_ctx* c, cudaStream_t s);
+cudaError_t launch_halo(hdgb_ctx* c, int mode, int plane, double* all, double* buf, cudaStream_t s);
+cudaError_t launch_pack(hdgb_ctx* c, int mode, const double* in, double* out, cudaStream_t s);
+cudaError_t enqueue_op_half(hdgb_ctx* c, int variant, cudaStream_t s);
+cudaError_t enqueue_update_half(hdgb_ctx* c, int prec, cudaStream_t s, cudaGraphConditionalHandle h, int has_loop);
 }  // namespace hdgb
 
 namespace hdgb {

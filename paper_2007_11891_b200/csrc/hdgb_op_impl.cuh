@@ -287,9 +287,11 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   constexpr bool PUPD = CG && (MODE & 8) && COLOR == 0;
   pdl_trigger();
   double beta = 0.0, alpha_prev = 0.0;
+  bool pwall = false;  // slab-group solve: <p, w> over both copies of interface faces
   if (CG) {
     pdl_wait();
     if (a.st->done) return;
+    pwall = a.st->dist != 0;
     if (PUPD) {
       beta = a.st->beta;
       alpha_prev = a.st->alpha;
@@ -542,7 +544,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       if (col == 1 && sh) val = prev[s] + val;
       if (CG && (col == 1 || !sh)) {  // final value of w here: Dirichlet row -> 0, <p, w>
         if (kinds[s] == HDGB_DIRICHLET) val = 0.0;
-        if (kind_counts(kinds[s])) dacc = fma(ur, val, dacc);
+        if (kind_counts_pw(kinds[s], pwall)) dacc = fma(ur, val, dacc);
       }
       a.r[off[s]] = val;
     };

@@ -21,7 +21,8 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["slab_range", "slab_side_kinds", "slab_mesh", "slab_local_index", "SlabHalo", "slab_pcg", "SlabSystem"]
+__all__ = ["slab_range", "slab_side_kinds", "slab_mesh", "slab_local_index", "SlabHalo", "slab_pcg", "SlabSystem",
+           "SlabGroup"]
 
 
 def slab_range(n1, rank, world):
@@ -233,3 +234,81 @@ class SlabSystem:
     def solve(self, F, x0, rtol=1e-10, atol=0.0, max_iters=10000):
         return slab_pcg(self.K, self.P if self.prec is not None else None, F, x0, self.dot, self._vec.axpby, rtol,
                         atol, max_iters, allreduce=lambda vals: _allreduce_sum(vals, self.group))
+
+
+class SlabGroup:
+    """The slabs of this process driven by the library (include/hdgb.h, hdgb_slab_*).
+
+    `dcs` are DeviceContexts of consecutive slabs [first_slab, first_slab + len(dcs)) of a job of
+    `nslabs` slabs (slab_mesh / slab_side_kinds), all on one device.  Neighbouring slabs inside
+    the process exchange interface planes in device memory; slabs of other processes over NCCL
+    (processes hold consecutive slab ranges, `proc` of `nprocs`; every process passes the same
+    `nccl_id`, see `nccl_unique_id` and `from_process_group`).  `apply` is hdg_op_3d with the
+    interface exchange, `pcg` the fused PCG (solver.py:282-321) of the whole job: per iteration
+    one exchange of w and two reductions, no host round trip inside a batch of 8 iterations.
+    """
+
+    def __init__(self, dcs, first_slab=0, nslabs=None, proc=0, nprocs=1, nccl_id=None):
+        import ctypes
+
+        self.dcs = list(dcs)
+        nslabs = len(self.dcs) if nslabs is None else nslabs
+        arr = (ctypes.c_void_p * len(self.dcs))(*[dc.handle.value if hasattr(dc.handle, "value") else dc.handle
+                                                   for dc in self.dcs])
+        h = ctypes.c_void_p()
+        idbuf = None if nccl_id is None else ctypes.create_string_buffer(bytes(nccl_id), 128)
+        _lib.check(_lib.lib().hdgb_slab_group_create(arr, len(self.dcs), int(first_slab), int(nslabs), int(proc),
+                                                     int(nprocs), idbuf, ctypes.byref(h)))
+        self.handle = h
+
+    @staticmethod
+    def nccl_unique_id():
+        """128-byte NCCL unique id (made by one process, broadcast to the others by the caller)."""
+        import ctypes
+
+        buf = ctypes.create_string_buffer(128)
+        _lib.check(_lib.lib().hdgb_nccl_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_process_group(cls, dcs, first_slab, nslabs, group=None):
+        """One group per process of the torch.distributed job; the NCCL id travels over `group`."""
+        import torch.distributed as dist
+
+        proc, nprocs = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.nccl_unique_id() if proc == 0 else None]
+        if nprocs > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(dcs, first_slab, nslabs, proc, nprocs, obj[0] if nprocs > 1 else None)
+
+    def _ptrs(self, tensors):
+        import ctypes
+
+        return (ctypes.c_void_p * len(self.dcs))(*[dc.check_vec(t).value for dc, t in zip(self.dcs, tensors)])
+
+    def apply(self, us, variant, out=None):
+        out = [dc.empty() for dc in self.dcs] if out is None else out
+        _lib.check(_lib.lib().hdgb_slab_apply(self.handle, int(variant), self._ptrs(us), self._ptrs(out),
+                                              self.dcs[0].stream()))
+        return out
+
+    def pcg(self, variant, prec, Fs, xs, rtol=1e-10, atol=0.0, max_iters=10000):
+        """x (per slab, in/out) of K x = F; returns (iterations, relative residual, converged)."""
+        import ctypes
+
+        it, rel, conv = ctypes.c_int32(), ctypes.c_double(), ctypes.c_int32()
+        _lib.check(_lib.lib().hdgb_slab_pcg(self.handle, int(variant), int(prec), self._ptrs(Fs), self._ptrs(xs),
+                                            float(rtol), float(atol), int(max_iters), ctypes.byref(it),
+                                            ctypes.byref(rel), ctypes.byref(conv), self.dcs[0].stream()))
+        return int(it.value), float(rel.value), bool(conv.value)
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            _lib.lib().hdgb_slab_group_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

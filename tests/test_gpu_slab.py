@@ -148,3 +148,72 @@ def test_nonuniform_slab_sides_rejected():
     mesh = hb.Mesh((2, 2, 2), widths=(np.array([0.3, 0.7]), np.array([0.5, 0.5]), np.array([0.5, 0.5])))
     with pytest.raises(ValueError, match="uniform grid"):
         DeviceContext(hb.Basis1D(3, 1.0), mesh, 1.0, side_kinds=slab_side_kinds(0, 2))
+
+
+# ---------------------------------------------------------------- library-driven slab groups
+from paper_2007_11891_b200.distributed import SlabGroup  # noqa: E402
+
+
+@pytest.mark.parametrize("world,p", [(2, 4), (3, 8)])
+def test_slab_group_apply_matches_global_oracle(world, p):
+    """hdgb_slab_apply: every slab's r equals the global hdg_op_3d(_transformed) on its faces,
+    interface copies included (operator.py:261-276)."""
+    gn = (7, 4, 3)
+    R = Ranks(gn, p, 0.9, 0.5, world)
+    octx = R.octx
+    u = np.random.default_rng(p).uniform(-1, 1, octx["grid"].n_all(octx["n"]))
+    G = SlabGroup(R.dcs)
+    for variant, tr in ((0, False), (1, True)):
+        ref = O.apply_op(octx, u, tr)
+        got = G.apply(R.scatter(u), variant)
+        for r in range(world):
+            assert relerr(got[r].cpu().numpy(), ref[R.idx[r]]) < TOL, (variant, r)
+    G.close()
+
+
+@pytest.mark.parametrize("p,world,variant,kind,nccl", [(3, 2, 0, 1, False), (8, 3, 0, 1, False), (4, 2, 1, 3, False),
+                                                        (13, 2, 0, 2, False), (5, 3, 1, 1, False), (4, 2, 0, 1, True)])
+def test_slab_group_pcg_matches_global_pcg(p, world, variant, kind, nccl):
+    """hdgb_slab_pcg (fused, CGState::dist, one exchange + two reductions per iteration) against
+    the single-context fused hdgb_pcg on the global grid: iterations within one, same solution
+    (solver.py:282-321).  nccl: the cross-process reductions through a one-process NCCL
+    communicator (ncclAllReduce captured in the iteration graphs)."""
+    gn = (6, 4, 3)
+    R = Ranks(gn, p, 0.9, 0.5, world)
+    octx = R.octx
+    grid, n = octx["grid"], octx["n"]
+    mask = grid.unknown_mask(n)
+    Fg = np.zeros(grid.n_all(n))
+    Fg[mask] = np.random.default_rng(p).uniform(-1, 1, int(mask.sum()))
+    gmesh = hb.Mesh(gn, (0, 0, 0), (1.5, 1.0, 1.0), BC)
+    gdc = DeviceContext(hb.Basis1D(p, 0.9), gmesh, 0.5)
+    xg = torch.zeros(grid.n_all(n), dtype=torch.float64, device="cuda")
+    itg, relg, convg = gdc.pcg(variant, kind, torch.from_numpy(Fg).cuda(), xg, 1e-10, 0.0, 1000)
+    G = SlabGroup(R.dcs, nccl_id=SlabGroup.nccl_unique_id() if nccl else None)
+    Fs = R.scatter(Fg)
+    xs = [torch.zeros_like(f) for f in Fs]
+    it, rel, conv = G.pcg(variant, kind, Fs, xs, rtol=1e-10, max_iters=1000)
+    assert conv and convg and abs(it - itg) <= 1, (it, itg)
+    assert rel <= 1e-10
+    xgn = xg.cpu().numpy()
+    for r in range(world):
+        assert relerr(xs[r].cpu().numpy(), xgn[R.idx[r]]) < 1e-9, r
+    # interface copies agree bitwise
+    for r in range(world - 1):
+        a, b = R.dcs[r], R.dcs[r + 1]
+        hi = SlabHalo._dev_pack(a, xs[r], a.mesh.n[0])
+        lo = SlabHalo._dev_pack(b, xs[r + 1], 0)
+        assert torch.equal(hi, lo)
+    # max_iters exhaustion and a second solve on the same group
+    xs2 = [torch.zeros_like(f) for f in Fs]
+    it2, rel2, conv2 = G.pcg(variant, kind, Fs, xs2, rtol=1e-10, max_iters=3)
+    assert it2 == 3 and not conv2 and rel2 > 1e-10
+    G.close()
+
+
+def test_slab_group_rejects_bad_layouts():
+    R = Ranks((6, 4, 3), 3, 0.9, 0.5, 2)
+    with pytest.raises(ValueError):
+        SlabGroup(R.dcs[::-1])  # interface kinds in the wrong order
+    with pytest.raises(ValueError):
+        SlabGroup(R.dcs[:1], first_slab=0, nslabs=2)  # a remote neighbour without NCCL
