@@ -16,8 +16,10 @@ transformed (Alg. 3) apply, the roofline of the operator kernel, and the CPU
 oracle timed on this host.
 
 Multi-GPU (torchrun, N > 1): weak scaling, each rank owns a 16^3 slab of a
-[0,N]x[0,1]^2 box (x-slab partition); the apply adds the NCCL halo exchange of
-the interface x-face planes.  `--impl reference` times the CPU oracle port of
+[0,N]x[0,1]^2 box (x-slab partition) as a library slab group (hdgb_slab_*): the
+apply adds the NCCL exchange of the interface x-face planes, the fused group
+PCG one exchange and two NCCL allreduces per iteration; `large.config5_xsplit`
+is BASELINE configs[4] (128^3, p = 8, split along x over the ranks).  `--impl reference` times the CPU oracle port of
 the reference path on rank 0 only.
 """
 
@@ -428,13 +430,12 @@ def _config4(hb, flush, stream, hbm, fp64_peak):
     return out
 
 
-def _distributed_cg(dc, halo, mesh, N, N_all, n, rank, world, stream):
-    """Distributed block-PCG: halo exchange in K, owned-face dots, two NCCL
-    allreduces per iteration; seeded RHS, consistent on the duplicated interface planes."""
+def _distributed_cg(dc, group, mesh, N, N_all, n, rank, world, stream):
+    """Distributed block-PCG through the library's slab group (hdgb_slab_pcg): per
+    iteration one interface exchange and two NCCL allreduces inside the iteration graphs; seeded
+    RHS, consistent on the duplicated interface planes."""
     import torch
     import torch.distributed as dist
-
-    from paper_2007_11891_b200.distributed import SlabSystem
 
     n2, n3 = mesh.n[1], mesh.n[2]
     l1 = mesh.n[0]
@@ -444,16 +445,16 @@ def _distributed_cg(dc, halo, mesh, N, N_all, n, rank, world, stream):
         fids = torch.arange(n2 * n3, device="cuda", dtype=torch.int64) * (l1 + 1)
         sel = (fids[:, None] * (n * n) + torch.arange(n * n, device="cuda")[None, :]).reshape(-1)
         Fd[sel] = 0.0
-    halo.exchange_add(Fd)
-    sysm = SlabSystem(dc, halo, variant=0, prec=1)
+    group.exchange([Fd])
     x0 = torch.zeros_like(Fd)
-    sysm.solve(Fd, x0, rtol=1e-10, max_iters=5)
+    group.pcg(0, 1, [Fd], [x0], rtol=1e-10, max_iters=5)
     torch.cuda.synchronize()
     dist.barrier()
+    x0.zero_()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record(stream)
-    _, it, rel, conv = sysm.solve(Fd, x0, rtol=1e-10, max_iters=500)
+    it, rel, conv = group.pcg(0, 1, [Fd], [x0], rtol=1e-10, max_iters=500)
     b.record(stream)
     b.synchronize()
     tt = torch.tensor([a.elapsed_time(b) * 1e-3], device="cuda", dtype=torch.float64)
@@ -462,8 +463,8 @@ def _distributed_cg(dc, halo, mesh, N, N_all, n, rank, world, stream):
     cg = {"preconditioner": "block (Alg. 4)", "iterations": it, "converged": conv, "relres": rel,
           "solve_ms": t_cg * 1e3, "ms_per_iter": t_cg / it * 1e3,
           "us_per_unknown_per_iter": t_cg / it / (world * N) * 1e6,
-          "note": "distributed.SlabSystem: host-driven recurrence, halo exchange per K, 2 NCCL allreduces "
-                  "per iteration; seeded uniform RHS"}
+          "note": "hdgb_slab_pcg: fused group PCG, one NCCL interface exchange + 2 NCCL allreduces per iteration "
+                  "inside CUDA graphs of 8 iterations; seeded uniform RHS"}
     return cg
 
 
@@ -475,21 +476,20 @@ def _config5_xsplit(hb, rank, world, local, stream, flush, steps=5):
     import torch
     import torch.distributed as dist
 
-    from paper_2007_11891_b200.distributed import SlabHalo, SlabSystem, slab_mesh, slab_side_kinds
+    from paper_2007_11891_b200.distributed import SlabGroup, slab_mesh, slab_side_kinds
 
     gn, p, lam = (128, 128, 128), 8, 1.0
     mesh = slab_mesh(gn, (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), rank, world)
     basis = hb.Basis1D(p, 25.0 * (1.0 / 128) / 2.0)
     dc = hb.DeviceContext(basis, mesh, lam, device=local, side_kinds=slab_side_kinds(rank, world))
-    halo = SlabHalo(dc, rank, world)
+    group = SlabGroup.from_process_group([dc], rank, world)
     gen = torch.Generator(device="cuda").manual_seed(5 + rank)
     u = torch.rand(dc.n_all, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
     dc.zero_dirichlet(u)
     r = dc.empty()
 
     def step():
-        dc.apply(u, 0, out=r)
-        halo.exchange_add(r)
+        group.apply([u], 0, out=[r])
 
     def timed(fn, reps):
         fn()
@@ -511,16 +511,23 @@ def _config5_xsplit(hb, rank, world, local, stream, flush, steps=5):
 
     N_glob = hb.Mesh(gn).n_trace_unknowns(p)
     t_apply = timed(step, steps)
-    sysm = SlabSystem(dc, halo, variant=0, prec=1)
     F = u.clone()
+    group.exchange([F])
     x0 = torch.zeros_like(F)
-    t_cg = timed(lambda: sysm.solve(F, x0, rtol=1e-300, max_iters=10), 2) / 10
+
+    def cg10():
+        x0.zero_()
+        group.pcg(0, 1, [F], [x0], rtol=1e-300, max_iters=16)
+
+    t_cg = timed(cg10, 2) / 16
     out = {"workload": "BASELINE configs[4]: 128^3 elements, p=8, lambda=1, split along x over the GPUs",
            "scaling": "strong", "trace_unknowns": N_glob, "apply_ms": t_apply * 1e3,
            "trace_dof_per_s": N_glob / t_apply, "pcg_ms_per_iter": t_cg * 1e3,
            "ps_per_unknown_per_iter": t_cg / N_glob * 1e12,
-           "note": "apply = local element passes + NCCL halo exchange of the interface x-face planes; PCG = "
-                   "distributed.SlabSystem (host-driven recurrence, two allreduces per iteration)"}
+           "note": "apply = local element passes + NCCL exchange of the interface x-face planes (hdgb_slab_apply); "
+                   "PCG = hdgb_slab_pcg, 16 block-PCG iterations (two graphs of 8), one exchange and two NCCL "
+                   "allreduces per iteration"}
+    group.close()
     del dc, u, r, F, x0
     torch.cuda.empty_cache()
     return out
@@ -563,16 +570,17 @@ def run_ours(args):
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
 
-    halo = None
+    group = None
     if world > 1:
-        from paper_2007_11891_b200.distributed import SlabHalo
+        from paper_2007_11891_b200.distributed import SlabGroup
 
-        halo = SlabHalo(dc, rank, world)
+        group = SlabGroup.from_process_group([dc], rank, world)
 
     def apply_step(variant):
-        dc.apply(u, variant, out=r)
-        if halo is not None:
-            halo.exchange_add(r)
+        if group is not None:
+            group.apply([u], variant, out=[r])
+        else:
+            dc.apply(u, variant, out=r)
 
     # ---- device-resident operator apply (value + roofline)
     steps, warm = args.steps, max(args.warmup, 3)
@@ -628,8 +636,7 @@ def run_ours(args):
             dc.apply_host_packed(hu, hr, 0)
         else:
             ud = h_u.to("cuda", non_blocking=True)
-            dc.apply(ud, 0, out=r)
-            halo.exchange_add(r)
+            group.apply([ud], 0, out=[r])
             h_r.copy_(r, non_blocking=True)
             torch.cuda.current_stream().synchronize()
 
@@ -724,7 +731,7 @@ def run_ours(args):
 
     if world > 1:
         try:
-            cg = _distributed_cg(dc, halo, mesh, N, N_all, n, rank, world, stream)
+            cg = _distributed_cg(dc, group, mesh, N, N_all, n, rank, world, stream)
         except Exception as exc:  # keep the apply line even if the solve fails on this box
             cg = {"error": f"{type(exc).__name__}: {exc}"}
         try:

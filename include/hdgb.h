@@ -187,6 +187,9 @@ int hdgb_slab_group_create(hdgb_ctx* const* ctxs, int nlocal, int first_slab, in
 int hdgb_slab_group_destroy(hdgb_slab_group* group);
 /* r = K u on every slab, interface planes exchanged (both copies hold the full residual). */
 int hdgb_slab_apply(hdgb_slab_group* group, int variant, const double* const* u, double* const* r, void* stream);
+/* vec[interface planes] += the neighbouring slabs' values there (the exchange of hdgb_slab_apply
+ * alone: a vector held as one-sided partials on the interfaces becomes consistent). */
+int hdgb_slab_exchange(hdgb_slab_group* group, double* const* vec, void* stream);
 /* Fused PCG over the group: per iteration one interface exchange of w and two reductions (local
  * fixed-order sums + ncclAllReduce), the rest as in hdgb_pcg; iterations run as CUDA graphs of 8
  * and the host reads the done flag of one batch while the next runs.  x is in/out per slab; the

@@ -80,6 +80,7 @@ SIGNATURES = {
     "hdgb_slab_group_create": (ctypes.c_int, [ctypes.POINTER(_VP), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                               ctypes.c_int, _VP, ctypes.POINTER(_VP)]),
     "hdgb_slab_group_destroy": (ctypes.c_int, [_VP]),
+    "hdgb_slab_exchange": (ctypes.c_int, [_VP, ctypes.POINTER(_VP), _VP]),
     "hdgb_slab_apply": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.POINTER(_VP), ctypes.POINTER(_VP), _VP]),
     "hdgb_slab_pcg": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_VP), ctypes.POINTER(_VP), _D, _D,
                                      _I32, ctypes.POINTER(_I32), ctypes.POINTER(_D), ctypes.POINTER(_I32), _VP]),

@@ -385,6 +385,17 @@ int hdgb_slab_apply(hdgb_slab_group* g, int variant, const double* const* u, dou
   return HDGB_OK;
 }
 
+int hdgb_slab_exchange(hdgb_slab_group* g, double* const* vec, void* stream) {
+  if (!g || !vec) return (set_error("null argument"), HDGB_EINVAL);
+  cudaStream_t us = (cudaStream_t)stream;
+  HDGB_CUDA(cudaEventRecord(g->ev, us));
+  HDGB_CUDA(cudaStreamWaitEvent(g->s, g->ev, 0));
+  HDGB_CUDA(exchange(g, vec, g->s));
+  HDGB_CUDA(cudaEventRecord(g->ev, g->s));
+  HDGB_CUDA(cudaStreamWaitEvent(us, g->ev, 0));
+  return HDGB_OK;
+}
+
 int hdgb_slab_pcg(hdgb_slab_group* g, int variant, int prec, const double* const* F, double* const* x, double rtol,
                   double atol, int32_t max_iters, int32_t* iters, double* relres, int32_t* converged, void* stream) {
   if (!g || !F || !x || !iters || !relres || !converged) return (set_error("null argument"), HDGB_EINVAL);

@@ -292,6 +292,11 @@ class SlabGroup:
                                               self.dcs[0].stream()))
         return out
 
+    def exchange(self, vecs):
+        """vec[interface planes] += the neighbouring slabs' values (in place)."""
+        _lib.check(_lib.lib().hdgb_slab_exchange(self.handle, self._ptrs(vecs), self.dcs[0].stream()))
+        return vecs
+
     def pcg(self, variant, prec, Fs, xs, rtol=1e-10, atol=0.0, max_iters=10000):
         """x (per slab, in/out) of K x = F; returns (iterations, relative residual, converged)."""
         import ctypes

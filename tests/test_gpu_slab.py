@@ -217,3 +217,16 @@ def test_slab_group_rejects_bad_layouts():
         SlabGroup(R.dcs[::-1])  # interface kinds in the wrong order
     with pytest.raises(ValueError):
         SlabGroup(R.dcs[:1], first_slab=0, nslabs=2)  # a remote neighbour without NCCL
+
+
+def test_slab_group_exchange_makes_interface_copies_consistent():
+    """hdgb_slab_exchange: one-sided interface values become the two-sided sums on both copies."""
+    R = Ranks((6, 4, 3), 4, 0.9, 0.5, 3)
+    G = SlabGroup(R.dcs)
+    vecs = [torch.from_numpy(np.random.default_rng(r).uniform(-1, 1, dc.n_all)).cuda() for r, dc in enumerate(R.dcs)]
+    ref = [v.clone() for v in vecs]
+    R.exchange_add(ref)
+    G.exchange(vecs)
+    for a, b in zip(vecs, ref):
+        assert torch.equal(a, b)
+    G.close()
