@@ -174,10 +174,16 @@ struct OpVCfg {
   // dz_inv lines in registers (N values per thread) up to N = 11; from a shared copy of the
   // table for N >= 12, where the registers are worth more (measured: p = 12 339 -> 312 us,
   // p = 16 490 -> 433 us; slower below)
+  // dz_inv computed per point on uniform grids too (1 / (lambda alpha0 + sum_d alpha_d Lambda),
+  // the non-uniform path's arithmetic): frees the N registers of the dz line
+#ifndef HDGB_OPV_DZCALC
+#define HDGB_OPV_DZCALC 0
+#endif
+  static constexpr bool DZC = HDGB_OPV_DZCALC;
 #ifdef HDGB_OPV_DZSMEM
-  static constexpr bool DZS = HDGB_OPV_DZSMEM;
+  static constexpr bool DZS = HDGB_OPV_DZSMEM && !DZC;
 #else
-  static constexpr bool DZS = N >= 12;
+  static constexpr bool DZS = N >= 12 && !DZC;
 #endif
   // PUPD (transformed PCG, direction and deferred x updates fused into colour pass 0): z and x
   // staged next to p, starting 16-byte aligned after the volume and the dz_inv copy
@@ -318,14 +324,15 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   const double b0a = FOLD ? K.B1[qa] : a.tab[to.BS + 2 * qa], b1a = FOLD ? 0.0 : a.tab[to.BS + 2 * qa + 1];
   const double b0b = FOLD ? K.B1[qb] : a.tab[to.BS + 2 * qb], b1b = FOLD ? 0.0 : a.tab[to.BS + 2 * qb + 1];
   const double lama = a.tab[to.Lam + qa], lamb = a.tab[to.Lam + qb];
-  constexpr bool DZR = UNI && !C::DZS;
+  constexpr bool DZR = UNI && !C::DZS && !C::DZC;
+  constexpr bool DZT = UNI && !C::DZC;  // dz_inv from the table (registers or shared)
   double dzr[DZR ? N : 1];
   double* sDz = smem + G * (2 * FS + VS);
   if (DZR) {
 #pragma unroll
     for (int a1 = 0; a1 < N; ++a1)  // dz_inv[a1][a2][a3] (FOLD: permuted a1)
       dzr[DZR ? a1 : 0] = __ldg(a.dz + (FOLD ? K.pNQ[a1] : a1 * NQ) + q);
-  } else if (UNI) {
+  } else if (UNI && C::DZS) {
     for (int i = tid; i < N * NQ; i += blockDim.x) {
       const int j1 = i / NQ, t = i - j1 * NQ;
       sDz[i] = __ldg(a.dz + (FOLD ? K.pNQ[j1] : j1 * NQ) + t);
@@ -552,7 +559,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       const double x0 = al1 * rw[0], x1 = al1 * rw[1];
       const double xs = x0 + x1, xd = x0 - x1;
       const double by = al2 * b0a, bz = al3 * b0b;
-      const double base = UNI ? 0.0 : a.lam * al0 + al2 * lama + al3 * lamb;
+      const double base = DZT ? 0.0 : a.lam * al0 + al2 * lama + al3 * lamb;
       double ex = 0.0, ox = 0.0;
 #pragma unroll
       for (int a1 = 0; a1 < N; ++a1) {
@@ -560,7 +567,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
         F = fma(by, ysel[K.pN[a1] + qb], F);
         F = fma(bz, zsel[K.pN[a1] + qa], F);
         const double dzv = DZR ? dzr[DZR ? a1 : 0]
-                               : (UNI ? sDz[a1 * NQ + q] : __drcp_rn(fma(al1, K.Lam[a1], base)));  // EigenScale3D
+                               : (DZT ? sDz[a1 * NQ + q] : __drcp_rn(fma(al1, K.Lam[a1], base)));  // EigenScale3D
         const double U = F * dzv;
         vU[K.pS1[a1] + qa * C::S2 + qb * C::S3] = U;
         if (a1 < NE) ex = fma(K.B0[a1], U, ex);
@@ -573,7 +580,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       const double xr0 = fb[0][q], xr1 = fb[1][q];
       const double x0 = al1 * xr0, x1 = al1 * xr1;
       const double by0 = al2 * b0a, by1 = al2 * b1a, bz0 = al3 * b0b, bz1 = al3 * b1b;
-      const double base = UNI ? 0.0 : a.lam * al0 + al2 * lama + al3 * lamb;
+      const double base = DZT ? 0.0 : a.lam * al0 + al2 * lama + al3 * lamb;
       double ax0 = 0.0, ax1 = 0.0;
 #pragma unroll
       for (int a1 = 0; a1 < N; ++a1) {
@@ -586,7 +593,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
         F = fma(bz0, z0, F);
         F = fma(bz1, z1, F);
         const double dzv = DZR ? dzr[DZR ? a1 : 0]
-                               : (UNI ? sDz[a1 * NQ + q] : __drcp_rn(fma(al1, K.Lam[a1], base)));  // EigenScale3D
+                               : (DZT ? sDz[a1 * NQ + q] : __drcp_rn(fma(al1, K.Lam[a1], base)));  // EigenScale3D
         const double U = F * dzv;
         vU[a1 * C::S1 + qa * C::S2 + qb * C::S3] = U;
         ax0 = fma(K.B0[a1], U, ax0);
