@@ -175,11 +175,15 @@ struct OpVCfg {
   // table for N >= 12, where the registers are worth more (measured: p = 12 339 -> 312 us,
   // p = 16 490 -> 433 us; slower below)
   // dz_inv computed per point on uniform grids too (1 / (lambda alpha0 + sum_d alpha_d Lambda),
-  // the non-uniform path's arithmetic): frees the N registers of the dz line
-#ifndef HDGB_OPV_DZCALC
-#define HDGB_OPV_DZCALC 0
-#endif
+  // the non-uniform path's arithmetic) instead of a shared copy of the N^3 table from N = 13:
+  // frees N^3 doubles of shared memory per CTA; transformed apply p = 12 276 -> 272, p = 13
+  // 328 -> 304, p = 14 397 -> 333, p = 15 312 -> 272, p = 16 374 -> 351 us (the DFMA pipe has
+  // room for the reciprocal); slower at N = 12 (p = 11 281 -> 322 us)
+#ifdef HDGB_OPV_DZCALC
   static constexpr bool DZC = HDGB_OPV_DZCALC;
+#else
+  static constexpr bool DZC = N >= 13;
+#endif
 #ifdef HDGB_OPV_DZSMEM
   static constexpr bool DZS = HDGB_OPV_DZSMEM && !DZC;
 #else
