@@ -383,6 +383,64 @@ def _config5_solve(hb, stream):
     return out
 
 
+def _config5_slabs_one_gpu(hb, stream, flush, nslab=2):
+    """BASELINE configs[4] x-split emulated on ONE GPU: the 128^3, p = 8, lambda = 1 grid as `nslab`
+    slab contexts in one process, driven by the library's slab group (interface exchange in device
+    memory, fused group PCG).  Same kernels and iteration graphs as the multi-GPU run minus NCCL:
+    measures the slab machinery (exchange, two reductions + decide kernels per iteration) at scale,
+    next to the single-context numbers of `config5_128^3_p8`."""
+    import torch
+
+    from paper_2007_11891_b200.distributed import SlabGroup, slab_mesh, slab_side_kinds
+
+    gn, p, lam = (128, 128, 128), 8, 1.0
+    basis = hb.Basis1D(p, 25.0 * (1.0 / 128) / 2.0)
+    dcs = [hb.DeviceContext(basis, slab_mesh(gn, (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), r, nslab), lam,
+                            side_kinds=slab_side_kinds(r, nslab)) for r in range(nslab)]
+    group = SlabGroup(dcs)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    us = [dc.zero_dirichlet(torch.rand(dc.n_all, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1)
+          for dc in dcs]
+    group.exchange(us)  # consistent interface copies
+    rs = [dc.empty() for dc in dcs]
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b) * 1e-3)
+        return statistics.median(ts)
+
+    N_glob = hb.Mesh(gn).n_trace_unknowns(p)
+    out = {"workload": f"BASELINE configs[4] grid split along x into {nslab} slab contexts on one GPU",
+           "trace_unknowns": N_glob}
+    for name, variant in (("plain", 0), ("transformed", 1)):
+        t = timed(lambda: group.apply(us, variant, out=rs), 5)
+        out[f"apply_{name}_ms"] = t * 1e3
+    xs = [torch.zeros_like(u) for u in us]
+    for name, variant, kind in (("block", 0, 1), ("transformed", 1, 3)):
+        def cg16():
+            for x in xs:
+                x.zero_()
+            group.pcg(variant, kind, us, xs, rtol=1e-300, max_iters=16)
+
+        out[f"pcg_{name}_ms_per_iter"] = timed(cg16, 2) / 16 * 1e3
+    out["note"] = ("hdgb_slab_apply / hdgb_slab_pcg (16 iterations = two graphs of 8); compare with "
+                   "config5_128^3_p8 (one context) for the cost of the slab exchange and the group reductions")
+    group.close()
+    del dcs, us, rs, xs
+    torch.cuda.empty_cache()
+    return out
+
+
 def _config4(hb, flush, stream, hbm, fp64_peak):
     """non-uniform 64x32x32 grid on [0,2]x[0,1]^2, p = 7, lambda = 100, per-axis
     widths uniform[0.5, 2] x mean from rng(7) (x, y, z order) rescaled to the box, tau_hat = 0.390625
@@ -796,6 +854,7 @@ def run_ours(args):
         if args.config5:
             large["config5_128^3_p8"] = _large_point(hb, 8, 128, 1.0, flush, stream, hbm, fp64_peak.value, reps=5)
             large["config5_128^3_p8"]["solve"] = _config5_solve(hb, stream)
+            large["config5_xsplit_2slabs_1gpu"] = _config5_slabs_one_gpu(hb, stream, flush)
 
     # ---- CPU oracle on this host (rank 0, N=1 only)
     cpu = None

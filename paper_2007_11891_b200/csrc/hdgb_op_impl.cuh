@@ -97,7 +97,8 @@ __device__ __forceinline__ void elem_alpha(const OpArgs& a, const int* c, double
 
 // PU: the colour-0 pass with the fused PCG direction update (MODE bits 0 and 3); FO: the
 // parity-folded kernel (MODE bit 4)
-template <int N, bool PU = false, bool FO = false>
+// CGT: the transformed operator in CG mode (Dirichlet rows, <p, w>)
+template <int N, bool PU = false, bool FO = false, bool CGT = false>
 struct OpVCfg {
   static constexpr int NQ = N * N;                      // threads (face positions) per element
 #ifndef HDGB_OPV_THREADS
@@ -179,10 +180,11 @@ struct OpVCfg {
   // frees N^3 doubles of shared memory per CTA; transformed apply p = 12 276 -> 272, p = 13
   // 328 -> 304, p = 14 397 -> 333, p = 15 312 -> 272, p = 16 374 -> 351 us (the DFMA pipe has
   // room for the reciprocal); slower at N = 12 (p = 11 281 -> 322 us)
+  // (not the transformed CG pass at N = 17: transformed PCG p = 16 781 -> 820 us/iter computed)
 #ifdef HDGB_OPV_DZCALC
   static constexpr bool DZC = HDGB_OPV_DZCALC;
 #else
-  static constexpr bool DZC = N >= 13;
+  static constexpr bool DZC = N >= 13 && !(N == 17 && CGT);
 #endif
 #ifdef HDGB_OPV_DZSMEM
   static constexpr bool DZS = HDGB_OPV_DZSMEM && !DZC;
@@ -285,7 +287,7 @@ template <int N, int MODE, int COLOR>
 __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
                                   OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::MINB) opV_kernel(const OpArgs a, int64_t t0, int64_t t1,
                                                           const __grid_constant__ OpVConst<N> K) {
-  using C = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, (MODE & 16) != 0>;
+  using C = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, (MODE & 16) != 0, (MODE & 5) == 1>;
   constexpr int NQ = C::NQ, G = C::G, FS = C::FS, VS = C::VS;
   constexpr bool UNI = !(MODE & 2), CG = MODE & 1, GONLY = MODE & 4, FOLD = MODE & 16;
   constexpr int NE = (N + 1) / 2;  // FOLD: even-class size (j < NE even)
@@ -727,7 +729,7 @@ static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
   if constexpr (!FOLD) {
     if (c->efold) return launch_passV<N, MODE | 16, COLOR>(c, a, t0, t1, s);
   }
-  using Cf = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, FOLD>;
+  using Cf = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, FOLD, (MODE & 5) == 1>;
   constexpr int SMD = (Cf::PREV && COLOR == 1) ? Cf::smem_doubles_prev(FOLD)
                      : (FOLD ? Cf::smem_doubles_fold() : Cf::smem_doubles((MODE & 9) == 9 && COLOR == 0));
   static_assert(sizeof(double) * SMD <= 227 * 1024, "element kernel shared memory exceeds 227 KB");
