@@ -234,6 +234,19 @@ def _cpu_sample(kind, times, threads):
             f"{statistics.median(times) * 1e3:.1f} ms; host {os.cpu_count()} cores")
 
 
+def _config_record(world, N, N_all):
+    """The `config` object of both arms (identical for the same N and world)."""
+    return {"workload": WORKLOAD if world == 1 else WORKLOAD + f"; per GPU, x-slab of a [0,{world}]x[0,1]^2 box",
+            "trace_unknowns_per_gpu": N, "all_face_dofs_per_gpu": N_all,
+            "l2": "flushed before every timed step (512 MB write)", "parallelism": f"x-slab dp{world}"}
+
+
+def _config2_all_face_dofs():
+    n1, n2, n3 = CFG["n_el"]
+    n = CFG["p"] + 1
+    return ((n1 + 1) * n2 * n3 + n1 * (n2 + 1) * n3 + n1 * n2 * (n3 + 1)) * n * n
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -247,7 +260,7 @@ def run_reference(args):
         "value": val, "unit": "trace-DOF/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1] trace vector)",
-        "config": {"workload": WORKLOAD, "trace_unknowns": N},
+        "config": _config_record(int(os.environ.get("WORLD_SIZE", "1")), N, _config2_all_face_dofs()),
         "cpu_baseline": {"value": val, "unit": "trace-DOF/s", "cores": cores, "kind": kind,
                          "sample": _cpu_sample(kind, times, cores)},
         "e2e": {"value": val, "unit": "trace-DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -899,9 +912,7 @@ def run_ours(args):
         "value": value, "unit": "trace-DOF/s", "n_gpus": world, "steps": steps, "warmup": warm,
         "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded uniform[-1,1] trace vector; manufactured sin RHS for CG)",
-        "config": {"workload": WORKLOAD if world == 1 else WORKLOAD + f"; per GPU, x-slab of a [0,{world}]x[0,1]^2 box",
-                   "trace_unknowns_per_gpu": N, "all_face_dofs_per_gpu": N_all,
-                   "l2": "flushed before every timed step (512 MB write)", "parallelism": f"x-slab dp{world}"},
+        "config": _config_record(world, N, N_all),
         "roofline": roofline,
         "fp64": fp64,
         "transformed_apply": {"value": N / t_tr, "unit": "trace-DOF/s", "kernel_ms": t_tr * 1e3,
