@@ -520,7 +520,8 @@ def _distributed_cg(dc, group, mesh, N, N_all, n, rank, world, stream):
     x0 = torch.zeros_like(Fd)
     group.pcg(0, 1, [Fd], [x0], rtol=1e-10, max_iters=5)
     torch.cuda.synchronize()
-    dist.barrier()
+    if dist.is_initialized():
+        dist.barrier()
     x0.zero_()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
@@ -529,7 +530,8 @@ def _distributed_cg(dc, group, mesh, N, N_all, n, rank, world, stream):
     b.record(stream)
     b.synchronize()
     tt = torch.tensor([a.elapsed_time(b) * 1e-3], device="cuda", dtype=torch.float64)
-    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    if dist.is_initialized():
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_cg = float(tt.item())
     cg = {"preconditioner": "block (Alg. 4)", "iterations": it, "converged": conv, "relres": rel,
           "solve_ms": t_cg * 1e3, "ms_per_iter": t_cg / it * 1e3,
@@ -565,7 +567,8 @@ def _config5_xsplit(hb, rank, world, local, stream, flush, steps=5):
     def timed(fn, reps):
         fn()
         torch.cuda.synchronize()
-        dist.barrier()
+        if dist.is_initialized():
+            dist.barrier()
         ts = []
         for _ in range(reps):
             flush.zero_()
@@ -577,7 +580,8 @@ def _config5_xsplit(hb, rank, world, local, stream, flush, steps=5):
             b.synchronize()
             ts.append(a.elapsed_time(b) * 1e-3)
         t = torch.tensor([statistics.median(ts)], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if dist.is_initialized():
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     N_glob = hb.Mesh(gn).n_trace_unknowns(p)
@@ -617,7 +621,10 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     p, n = CFG["p"], CFG["p"] + 1
     large = {}
-    if world > 1:
+    # --slab-path: the N > 1 code path (slab group, exchange, group PCG, config-5 x-split) on one
+    # process, as a one-slab job (test hook for the multi-GPU bench without a multi-GPU box)
+    multi = world > 1 or args.slab_path
+    if multi:
         import paper_2007_11891_b200 as hb
         from paper_2007_11891_b200.distributed import slab_mesh, slab_side_kinds
 
@@ -633,7 +640,7 @@ def run_ours(args):
         hb, mesh, cfg, ctx = build_problem()
         N_global = mesh.n_trace_unknowns(p)
     dc = hb.device_context(ctx)
-    N = mesh.n_trace_unknowns(p) if world == 1 else N_global // world
+    N = mesh.n_trace_unknowns(p) if not multi else N_global // world
     N_all = mesh.n_all(p)
     v = np.random.default_rng(1 + rank).uniform(-1.0, 1.0, dc.n_unknown)
     u = dc.unpack(torch.from_numpy(v).cuda())
@@ -642,7 +649,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     group = None
-    if world > 1:
+    if multi:
         from paper_2007_11891_b200.distributed import SlabGroup
 
         group = SlabGroup.from_process_group([dc], rank, world)
@@ -697,13 +704,13 @@ def run_ours(args):
 
     # ---- e2e through the C ABI with pinned host buffers: the reference's apply_K closure on
     # packed unknown vectors (hdgb_op_apply_host_packed: H2D, unpack, apply, pack, D2H, sync)
-    n_e2e = dc.n_unknown if world == 1 else N_all
+    n_e2e = dc.n_unknown if not multi else N_all
     h_u = torch.empty(n_e2e, dtype=torch.float64).pin_memory()
     h_r = torch.empty(n_e2e, dtype=torch.float64).pin_memory()
-    h_u.copy_(dc.pack(u).cpu() if world == 1 else u.cpu())
+    h_u.copy_(dc.pack(u).cpu() if not multi else u.cpu())
     hu, hr = h_u.numpy(), h_r.numpy()
     def e2e_step():
-        if world == 1:
+        if not multi:
             dc.apply_host_packed(hu, hr, 0)
         else:
             ud = h_u.to("cuda", non_blocking=True)
@@ -744,12 +751,12 @@ def run_ours(args):
             "affinity": affinity}
     e2e_step()  # h_r holds the apply again (checked below)
     apply_step(0)
-    ref_e2e = dc.pack(r).cpu().numpy() if world == 1 else r.cpu().numpy()
+    ref_e2e = dc.pack(r).cpu().numpy() if not multi else r.cpu().numpy()
     assert np.array_equal(hr, ref_e2e), "e2e result differs from the device-resident apply"
 
     # ---- fused block-PCG solve (CG us per unknown per iteration)
     cg = None
-    if world == 1:
+    if not multi:
         F = _sin_rhs(hb, mesh, ctx)
         Fd = dc.unpack(torch.from_numpy(F).cuda())
         x = torch.zeros_like(Fd)
@@ -800,7 +807,7 @@ def run_ours(args):
                              "ms_per_iter": t_tr_cg / it_t * 1e3,
                              "us_per_unknown_per_iter": t_tr_cg / it_t / N * 1e6}
 
-    if world > 1:
+    if multi:
         try:
             cg = _distributed_cg(dc, group, mesh, N, N_all, n, rank, world, stream)
         except Exception as exc:  # keep the apply line even if the solve fails on this box
@@ -947,6 +954,8 @@ def main():
     ap.add_argument("--sweep", action="store_true", help="full config-3 degree sweep p=2..16")
     ap.add_argument("--config4", action="store_true", help="also time config 4 (64x32x32 non-uniform, p=7)")
     ap.add_argument("--config5", action="store_true", help="also time config 5 (128^3, p=8, 4 GB vectors)")
+    ap.add_argument("--slab-path", action="store_true",
+                    help="test hook: run the multi-GPU code path (slab group) as a one-slab job on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

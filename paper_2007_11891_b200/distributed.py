@@ -275,6 +275,8 @@ class SlabGroup:
         """One group per process of the torch.distributed job; the NCCL id travels over `group`."""
         import torch.distributed as dist
 
+        if not (dist.is_available() and dist.is_initialized()):
+            return cls(dcs, first_slab, nslabs)  # a one-process job
         proc, nprocs = dist.get_rank(group), dist.get_world_size(group)
         obj = [cls.nccl_unique_id() if proc == 0 else None]
         if nprocs > 1:
