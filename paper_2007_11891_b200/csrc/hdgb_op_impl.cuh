@@ -206,6 +206,21 @@ struct OpVCfg {
   // with the faces, one group ahead (2 x G x [6][FSTR] after everything else)
   // (N >= 6: p = 5..11 and 16 2-5 % faster; smaller N lose the occupancy to the extra buffer)
   static constexpr bool PREV = !TMA && !PU && N >= 6;
+  // register staging (folded kernel, cp.async shapes, no fused direction update): every thread
+  // only ever reads back the six face values it staged itself, so it loads them (and the
+  // colour-0 partials) straight into registers one group ahead instead of through shared memory;
+  // the folded y / z faces get one buffer of 4 FSF doubles per element (no raw buffers)
+#ifndef HDGB_OPV_RS
+#define HDGB_OPV_RS 1
+#endif
+  static constexpr bool RS = HDGB_OPV_RS && FO && !TMA && !PU;
+  // colour-0 partials under RS: 1 = in registers one group ahead, 2 = loaded at the top of their
+  // own group (consumed at the emits)
+#ifndef HDGB_OPV_RSP
+#define HDGB_OPV_RSP 2
+#endif
+  static constexpr bool RSP1 = HDGB_OPV_RSP == 1;
+  __host__ __device__ static constexpr int smem_doubles_rs() { return G * (4 * FSF + VS) + (DZS ? N * NQ : 0); }
   __host__ __device__ static constexpr int smem_doubles_prev(bool fold) { return (fold ? smem_doubles_fold() : smem_doubles(PU)) + 2 * G * FS; }
   __host__ __device__ static constexpr int POFF(bool fold) { return fold ? smem_doubles_fold() : smem_doubles(PU); }
 };
@@ -313,8 +328,9 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   constexpr int FSTR = C::FSTR;
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) uint64_t sBar[2];  // TMA: one transaction barrier per staging buffer
-  double* sF0 = smem;              // 2 x G x [6][FSTR] staged faces
-  double* sU = smem + 2 * G * FS;  // G x [N][NQ] volume
+  constexpr bool RS = C::RS && COLOR != 2;  // faces (and colour-0 partials) staged in registers
+  double* sF0 = smem;              // 2 x G x [6][FSTR] staged faces (RS: G x [4][FSF] folded faces)
+  double* sU = smem + (RS ? G * 4 * C::FSF : 2 * G * FS);  // G x [N][NQ] volume
   // element records of groups k .. k + 3 (prefetched three groups ahead, slot k % 4)
   __shared__ ERec sRec[4][G];
   __shared__ __align__(16) double sAl[4][G][4];  // non-uniform: alpha0..3
@@ -333,7 +349,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   constexpr bool DZR = UNI && !C::DZS && !C::DZC;
   constexpr bool DZT = UNI && !C::DZC;  // dz_inv from the table (registers or shared)
   double dzr[DZR ? N : 1];
-  double* sDz = smem + G * (2 * FS + VS);
+  double* sDz = sU + G * VS;
   if (DZR) {
 #pragma unroll
     for (int a1 = 0; a1 < N; ++a1)  // dz_inv[a1][a2][a3] (FOLD: permuted a1)
@@ -379,7 +395,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       else *dst = __ldg(src);
     }
   };
-  constexpr bool PREV = C::PREV && COLOR == 1;  // colour-0 partials staged with the faces
+  constexpr bool PREV = C::PREV && COLOR == 1 && !RS;  // colour-0 partials staged with the faces
   double* sP0 = smem + C::POFF(FOLD);            // PREV: 2 x G x [6][FSTR] staged partials
   double* sZ0 = smem + C::ZOFF;      // PUPD: 2 x G x [6][FSTR] staged z
   double* sX0 = sZ0 + 2 * G * FS;    // PUPD: 2 x G x [6][FSTR] staged x
@@ -453,6 +469,27 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     }
   };
 
+  // RS: position q of the six faces of group kk (colour pass 1: and the colour-0 partials of
+  // its shared faces) into registers, consumed one iteration later
+  double nxt[RS ? 6 : 1], nprv[(RS && COLOR == 1 && C::RSP1) ? 6 : 1];
+  // `dep` (always 0) is derived from the values of the current group: ptxas otherwise hoists
+  // these loads above the first use of the current values, which then waits on a scoreboard the
+  // new loads share (ncu: one DADD with 32 % of the stall samples)
+  auto rs_issue = [&](int64_t kk, unsigned dep) {
+    if constexpr (RS) {
+      const uint4* R = reinterpret_cast<const uint4*>(&sRec[kk & 3][act ? e : 0]);
+      const uint4 w0 = R[0], w1 = R[1];
+      const uint32_t o[6] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y};
+      const bool ok = act && kk < nslots && (w1.z & 1u);
+      const unsigned qd = (unsigned)q + dep;
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        nxt[s] = ok ? __ldcg(a.u + (o[s] + qd)) : 0.0;
+        if constexpr (COLOR == 1 && C::RSP1) nprv[s] = (ok && (w1.z >> (1 + s) & 1u)) ? __ldcg(a.r + (o[s] + qd)) : 0.0;
+      }
+    }
+  };
+
   double dacc = 0.0;  // CG: this thread's share of <p, w> (fixed grid -> reproducible)
   int64_t verified = -1;  // merged schedule: colour-0 waves known complete (thread 0)
   // records of groups 0..2 now; group k + 3's is fetched with the faces of group k + 1, so it
@@ -463,12 +500,16 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   fetch(2, false);
   __syncthreads();
   if (!CG) pdl_wait();  // u and r come from earlier kernels
-  if (nslots > 0) stage(sRec[0], sF0, 0);
+  if (RS) rs_issue(0, 0u);
+  else if (nslots > 0) stage(sRec[0], sF0, 0);
   cp_async_commit();
   for (int64_t k = 0; k < nslots; ++k) {
     const int buf = (int)(k & 1);
-    __syncthreads();
-    if (k + 1 < nslots) stage(sRec[(k + 1) & 3], sF0 + (buf ^ 1) * G * FS, buf ^ 1);
+    // RS: no barrier here (the folded faces of group k - 1 were last read before its phase
+    // barrier, record k + 1 was published by the barriers of iteration k - 1, and slot
+    // (k + 3) & 3 held record k - 1, last read at the top of iteration k - 1)
+    if (!RS) __syncthreads();
+    if (!RS && k + 1 < nslots) stage(sRec[(k + 1) & 3], sF0 + (buf ^ 1) * G * FS, buf ^ 1);
     if (k + 3 < nslots) fetch(k + 3, true);
     cp_async_commit();
     asm volatile("cp.async.wait_group 1;\n" ::);
@@ -484,14 +525,16 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       verified = need > verified ? need : verified;
     }
     // element geometry into registers once (record k was published two barriers ago)
-    const ERec& I = sRec[k & 3][act ? e : 0];
-    const uint32_t flags = I.flags;
+    const uint4* Iw = reinterpret_cast<const uint4*>(&sRec[k & 3][act ? e : 0]);  // two 128-bit reads
+    const uint4 i0 = Iw[0], i1 = Iw[1];
+    const uint32_t roff[6] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y};
+    const uint32_t flags = i1.z;
     const bool on = act && (flags & 1u);
     unsigned off[6];
     int kinds[6];
 #pragma unroll
     for (int s2 = 0; s2 < 6; ++s2) {
-      off[s2] = I.off[s2] + (unsigned)q;
+      off[s2] = roff[s2] + (unsigned)q;
       kinds[s2] = CG ? (int)(flags >> (8 + 3 * s2) & 7u) : 0;
     }
     const unsigned shared = flags >> 1 & 63u;
@@ -500,7 +543,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     double* sFw = sF0 + buf * G * FS + (act ? e : 0) * FS;
     double* fb[6];  // face s of the element: fb[s][position]
 #pragma unroll
-    for (int s2 = 0; s2 < 6; ++s2) fb[s2] = sFw + s2 * FSTR + ((TMA && (NQ & 1)) ? (I.off[s2] & 1u) : 0u);
+    for (int s2 = 0; s2 < 6; ++s2) fb[s2] = sFw + s2 * FSTR + ((TMA && (NQ & 1)) ? (roff[s2] & 1u) : 0u);
     double* vU = sU + (act ? e : 0) * VS;
     const int own = q;  // this thread's face position
     if (PUPD && on) {  // position q of every face is this thread's own copy (cp.async) or
@@ -519,19 +562,40 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     }
     // FOLD: raw own values (self terms, <p, w>) into registers, folded y / z faces out
     double rw[6];
+    double prev[6];  // colour-0 partials of the shared faces at q (colour pass 1)
+    if constexpr (RS) {  // this group's values arrive (issued one iteration ago); the next group's leave
+#pragma unroll
+      for (int s = 0; s < 6; ++s) rw[s] = nxt[s];
+      if constexpr (COLOR == 1) {
+#pragma unroll
+        for (int s = 0; s < 6; ++s) {
+          if constexpr (C::RSP1) prev[s] = nprv[s];
+          else prev[s] = (on && (shared >> s & 1u)) ? __ldcg(a.r + off[s]) : 0.0;
+        }
+      }
+      unsigned dep = 0;
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        dep |= (unsigned)__double2hiint(rw[s]);
+        if constexpr (COLOR == 1 && C::RSP1) dep |= (unsigned)__double2hiint(prev[s]);
+      }
+      rs_issue(k + 1, dep & i1.w);  // i1.w: the record's spare word, always 0
+    }
     // folded faces in permuted order: y (sum / difference of the two sides) [j1][j3], z [j1][j2];
     // phase 1 reads the class of its own a2 (y) and a3 (z)
     const double* ysel = nullptr;
     const double* zsel = nullptr;
     if (FOLD) {
-      double* fo = TMA ? smem + C::FOFF + (act ? e : 0) * 4 * C::FSF : nullptr;
-      double* ys = TMA ? fo : fb[2];
-      double* yd = TMA ? fo + C::FSF : fb[3];
-      double* zs = TMA ? fo + 2 * C::FSF : fb[4];
-      double* zd = TMA ? fo + 3 * C::FSF : fb[5];
+      double* fo = (TMA || RS) ? smem + (RS ? 0 : C::FOFF) + (act ? e : 0) * 4 * C::FSF : nullptr;
+      double* ys = (TMA || RS) ? fo : fb[2];
+      double* yd = (TMA || RS) ? fo + C::FSF : fb[3];
+      double* zs = (TMA || RS) ? fo + 2 * C::FSF : fb[4];
+      double* zd = (TMA || RS) ? fo + 3 * C::FSF : fb[5];
       if (on) {
+        if (!RS) {
 #pragma unroll
-        for (int s = 0; s < 6; ++s) rw[s] = fb[s][own];
+          for (int s = 0; s < 6; ++s) rw[s] = fb[s][own];
+        }
         ys[q] = rw[2] + rw[3];
         yd[q] = rw[2] - rw[3];
         zs[q] = rw[4] + rw[5];
@@ -542,8 +606,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     }
     __syncthreads();  // staged faces (and their update) visible to the whole CTA
     // colour-0 partials of the shared faces at q: issued now, consumed at the emits
-    double prev[6];
-    if (col == 1 && on) {
+    if (!RS && col == 1 && on) {
       const double* sP = sP0 + buf * G * FS + (act ? e : 0) * FS + q;
 #pragma unroll
       for (int s = 0; s < 6; ++s)
@@ -730,7 +793,8 @@ static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
     if (c->efold) return launch_passV<N, MODE | 16, COLOR>(c, a, t0, t1, s);
   }
   using Cf = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, FOLD, (MODE & 5) == 1>;
-  constexpr int SMD = (Cf::PREV && COLOR == 1) ? Cf::smem_doubles_prev(FOLD)
+  constexpr int SMD = (Cf::RS && COLOR != 2) ? Cf::smem_doubles_rs()
+                     : (Cf::PREV && COLOR == 1) ? Cf::smem_doubles_prev(FOLD)
                      : (FOLD ? Cf::smem_doubles_fold() : Cf::smem_doubles((MODE & 9) == 9 && COLOR == 0));
   static_assert(sizeof(double) * SMD <= 227 * 1024, "element kernel shared memory exceeds 227 KB");
   const size_t smem = sizeof(double) * (size_t)SMD;
