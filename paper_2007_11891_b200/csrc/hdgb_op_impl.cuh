@@ -213,14 +213,19 @@ struct OpVCfg {
 #ifndef HDGB_OPV_RS
 #define HDGB_OPV_RS 1
 #endif
-  static constexpr bool RS = HDGB_OPV_RS && FO && !TMA && !PU;
+#ifndef HDGB_OPV_RSPU
+#define HDGB_OPV_RSPU 1
+#endif
+  // (with the fused direction update, PU: p in registers, z and x still through cp.async slots)
+  static constexpr bool RS = HDGB_OPV_RS && FO && !TMA && (!PU || HDGB_OPV_RSPU);
   // colour-0 partials under RS: 1 = in registers one group ahead, 2 = loaded at the top of their
   // own group (consumed at the emits)
 #ifndef HDGB_OPV_RSP
 #define HDGB_OPV_RSP 2
 #endif
-  static constexpr bool RSP1 = HDGB_OPV_RSP == 1;
-  __host__ __device__ static constexpr int smem_doubles_rs() { return G * (4 * FSF + VS) + (DZS ? N * NQ : 0); }
+  static constexpr bool RSP1 = HDGB_OPV_RSP == 1;  // measured: 2 is 1-14 % faster for p = 3..11 except p = 7 (4 % slower)
+  static constexpr int ZOFF_RS = (G * (4 * FSF + VS) + (DZS ? N * NQ : 0) + 1) / 2 * 2;
+  __host__ __device__ static constexpr int smem_doubles_rs() { return PU ? ZOFF_RS + 4 * G * FS : G * (4 * FSF + VS) + (DZS ? N * NQ : 0); }
   __host__ __device__ static constexpr int smem_doubles_prev(bool fold) { return (fold ? smem_doubles_fold() : smem_doubles(PU)) + 2 * G * FS; }
   __host__ __device__ static constexpr int POFF(bool fold) { return fold ? smem_doubles_fold() : smem_doubles(PU); }
 };
@@ -397,7 +402,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   };
   constexpr bool PREV = C::PREV && COLOR == 1 && !RS;  // colour-0 partials staged with the faces
   double* sP0 = smem + C::POFF(FOLD);            // PREV: 2 x G x [6][FSTR] staged partials
-  double* sZ0 = smem + C::ZOFF;      // PUPD: 2 x G x [6][FSTR] staged z
+  double* sZ0 = smem + (RS ? C::ZOFF_RS : C::ZOFF);  // PUPD: 2 x G x [6][FSTR] staged z
   double* sX0 = sZ0 + 2 * G * FS;    // PUPD: 2 x G x [6][FSTR] staged x
   if (TMA && tid == 0) {
     mbar_init(&sBar[0], 1);
@@ -449,8 +454,10 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     }
     if (act && (inf[e].flags & 1u)) {
       double* dst = buf + e * FS + q;
+      if (!RS) {
 #pragma unroll
-      for (int s = 0; s < 6; ++s) cp_async8(dst + s * FSTR, a.u + (inf[e].off[s] + (unsigned)q));
+        for (int s = 0; s < 6; ++s) cp_async8(dst + s * FSTR, a.u + (inf[e].off[s] + (unsigned)q));
+      }
       if (PREV) {
         const uint32_t sh = inf[e].flags >> 1;
         double* dp = sP0 + bi * G * FS + e * FS + q;
@@ -501,7 +508,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   __syncthreads();
   if (!CG) pdl_wait();  // u and r come from earlier kernels
   if (RS) rs_issue(0, 0u);
-  else if (nslots > 0) stage(sRec[0], sF0, 0);
+  if ((!RS || PUPD) && nslots > 0) stage(sRec[0], sF0, 0);
   cp_async_commit();
   for (int64_t k = 0; k < nslots; ++k) {
     const int buf = (int)(k & 1);
@@ -509,7 +516,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     // barrier, record k + 1 was published by the barriers of iteration k - 1, and slot
     // (k + 3) & 3 held record k - 1, last read at the top of iteration k - 1)
     if (!RS) __syncthreads();
-    if (!RS && k + 1 < nslots) stage(sRec[(k + 1) & 3], sF0 + (buf ^ 1) * G * FS, buf ^ 1);
+    if ((!RS || PUPD) && k + 1 < nslots) stage(sRec[(k + 1) & 3], sF0 + (buf ^ 1) * G * FS, buf ^ 1);
     if (k + 3 < nslots) fetch(k + 3, true);
     cp_async_commit();
     asm volatile("cp.async.wait_group 1;\n" ::);
@@ -546,7 +553,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     for (int s2 = 0; s2 < 6; ++s2) fb[s2] = sFw + s2 * FSTR + ((TMA && (NQ & 1)) ? (roff[s2] & 1u) : 0u);
     double* vU = sU + (act ? e : 0) * VS;
     const int own = q;  // this thread's face position
-    if (PUPD && on) {  // position q of every face is this thread's own copy (cp.async) or
+    if (PUPD && !RS && on) {  // position q of every face is this thread's own copy (cp.async) or
                        // complete for every thread (TMA barrier): no extra CTA barrier needed
       const double* sZ = sZ0 + buf * G * FS + (act ? e : 0) * FS;
       const double* sX = sX0 + buf * G * FS + (act ? e : 0) * FS;
@@ -580,6 +587,17 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
         if constexpr (COLOR == 1 && C::RSP1) dep |= (unsigned)__double2hiint(prev[s]);
       }
       rs_issue(k + 1, dep & i1.w);  // i1.w: the record's spare word, always 0
+      if (PUPD && on) {  // direction and deferred x updates at this thread's six positions
+        const double* sZ = sZ0 + buf * G * FS + e * FS + q;
+        const double* sX = sX0 + buf * G * FS + e * FS + q;
+#pragma unroll
+        for (int s = 0; s < 6; ++s) {
+          const double po = rw[s], pn = fma(beta, po, sZ[s * FSTR]);
+          rw[s] = pn;
+          a.pout[off[s]] = pn;
+          a.xout[off[s]] = fma(alpha_prev, po, sX[s * FSTR]);
+        }
+      }
     }
     // folded faces in permuted order: y (sum / difference of the two sides) [j1][j3], z [j1][j2];
     // phase 1 reads the class of its own a2 (y) and a3 (z)
@@ -624,6 +642,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       }
       a.r[off[s]] = val;
     };
+    double gx0 = 0.0, gx1 = 0.0;
     if (FOLD && on) {  // phase 1, folded: x-line of (a2, a3) = (qa, qb), a1 = perm[j] in class order
       const double x0 = al1 * rw[0], x1 = al1 * rw[1];
       const double xs = x0 + x1, xd = x0 - x1;
@@ -642,8 +661,13 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
         if (a1 < NE) ex = fma(K.B0[a1], U, ex);
         else ox = fma(K.B0[a1], U, ox);
       }
-      emit(0, al1 * (ex + ox), x0, rw[0]);
-      emit(1, al1 * (ex - ox), x1, rw[1]);
+      if constexpr (RS && COLOR == 1) {  // x faces emitted after phase 2: the partials loaded at the top get a whole group to arrive
+        gx0 = al1 * (ex + ox);
+        gx1 = al1 * (ex - ox);
+      } else {
+        emit(0, al1 * (ex + ox), x0, rw[0]);
+        emit(1, al1 * (ex - ox), x1, rw[1]);
+      }
     }
     if (!FOLD && on) {  // phase 1: x-line of (a2, a3) = (qa, qb)
       const double xr0 = fb[0][q], xr1 = fb[1][q];
@@ -705,6 +729,10 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       }
       const double yr0 = FOLD ? rw[2] : fb[2][q], yr1 = FOLD ? rw[3] : fb[3][q];
       const double zr0 = FOLD ? rw[4] : fb[4][q], zr1 = FOLD ? rw[5] : fb[5][q];
+      if constexpr (FOLD && RS && COLOR == 1) {
+        emit(0, gx0, al1 * rw[0], rw[0]);
+        emit(1, gx1, al1 * rw[1], rw[1]);
+      }
       emit(2, al2 * ay0, al2 * yr0, yr0);
       emit(3, al2 * ay1, al2 * yr1, yr1);
       emit(4, al3 * az0, al3 * zr0, zr0);

@@ -52,6 +52,30 @@ def main():
             chk = float(r.double().abs().sum().item())
             print(f"p={p} m={m} variant={variant} us={t:.1f} min={min(ts):.1f} frac16={16 * N / t / 1e3 / hbm:.3f} "
                   f"sum|r|={chk:.12e}", flush=True)
+        if os.environ.get("HDGB_PROBE_PCG", "1") != "0":
+            F = r.clone()
+            F.copy_(u)
+            dc.zero_dirichlet(F)
+            x = torch.zeros_like(F)
+            iters = 10
+            for name, variant, kind in (("pcg_block", 0, 1), ("pcg_transformed", 1, 3)):
+                x.zero_()
+                dc.pcg(variant, kind, F, x, 1e-300, 0.0, iters)
+                ts = []
+                for _ in range(3):
+                    flush.zero_()
+                    x.zero_()
+                    a = torch.cuda.Event(enable_timing=True)
+                    b = torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    it, _, _ = dc.pcg(variant, kind, F, x, 1e-300, 0.0, iters)
+                    b.record(stream)
+                    b.synchronize()
+                    ts.append(a.elapsed_time(b) * 1e3)
+                t_it = statistics.median(ts) / max(it, 1)
+                print(f"p={p} {name} us_per_iter={t_it:.1f} frac96={96 * N / t_it / 1e3 / hbm:.3f} "
+                      f"sum|x|={float(x.abs().sum().item()):.12e}", flush=True)
+            del F, x
         del dc, u, r
 
 
