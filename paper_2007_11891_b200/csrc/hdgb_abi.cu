@@ -98,7 +98,10 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
   c->dev = d->device;
   if (const char* sb = getenv("HDGB_SLAB_MB")) c->slab_bytes = (int64_t)atof(sb) * (1LL << 20);
   if (const char* gc = getenv("HDGB_GRID_CAP")) c->grid_cap = atoll(gc);
-  c->merge = d->p + 1 >= 17;
+  // merged colour schedule: was the default at N = 17 until the element kernel staged its faces
+  // in registers (separate passes only): p = 16 transformed apply 343 -> 323 us, transformed PCG
+  // 821 -> 688 us/iter unmerged
+  c->merge = 0;
   if (const char* mg = getenv("HDGB_MERGE")) c->merge = atoi(mg);
   if (const char* ms = getenv("HDGB_MERGE_SLACK")) c->merge_slack = atoi(ms);
   if (const char* mb = getenv("HDGB_MERGE_BATCH")) c->merge_batch = atoi(mb) > 0 ? atoi(mb) : 1;
@@ -310,7 +313,9 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
     // default per degree (config-3 sweep, transformed apply at ~2e7 unknowns): folded faster at
     // p = 3 (160 vs 174 us), 8 (246 vs 252), 12 (275 vs 288), 16 (374 vs 414); slower at p = 2
     // (296 vs 202) and p = 4 (236 vs 200); HDGB_EFOLD=1 forces it on, =0 off
-    const bool efdef = N == 4 || N >= 6;
+    // (with register-staged faces the folded kernel also wins at p = 2: 194 -> 183 us; p = 4
+    // stays unfolded: 196 vs 222 us)
+    const bool efdef = N == 3 || N == 4 || N >= 6;
     c->efold = ok && neven == (N + 1) / 2 && dev <= 2.5e-12 * bmx && !(ef && atoi(ef) == 0) &&
                (efdef || (ef && atoi(ef) == 1));
     if (c->efold) {

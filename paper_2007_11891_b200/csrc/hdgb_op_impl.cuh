@@ -142,7 +142,11 @@ struct OpVCfg {
 #ifndef HDGB_OPV_TMA_NMAX
 #define HDGB_OPV_TMA_NMAX 16
 #endif
-  static constexpr bool TMA = N >= HDGB_OPV_TMA_NMIN && N <= HDGB_OPV_TMA_NMAX;
+  // (round 2: with register-staged faces the cp.async shapes win back N = 13 and 15: transformed
+  // apply p = 12 265 -> 239 us, p = 14 324 -> 310 us, transformed PCG 720 -> 651 and 793 -> 763
+  // us/iter; N = 14 mixed (apply 265 vs 275, transformed PCG 804 vs 770), N = 16 keeps the
+  // bulk copies: 263 vs 277 us)
+  static constexpr bool TMA = N >= HDGB_OPV_TMA_NMIN && N <= HDGB_OPV_TMA_NMAX && !(N & 1);
   // folded kernel: the even- and odd-class folded faces (sum / difference of the two sides) are
   // read side by side by lanes of either class; slots FSF doubles apart with FSF mod 16 in
   // [N, 16 - N] (N <= 8: disjoint banks) or = N (N = 9..15: nearly so) avoid bank conflicts
@@ -333,7 +337,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   constexpr int FSTR = C::FSTR;
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) uint64_t sBar[2];  // TMA: one transaction barrier per staging buffer
-  constexpr bool RS = C::RS && COLOR != 2;  // faces (and colour-0 partials) staged in registers
+  constexpr bool RS = C::RS;  // faces (and colour-0 partials) staged in registers
   double* sF0 = smem;              // 2 x G x [6][FSTR] staged faces (RS: G x [4][FSF] folded faces)
   double* sU = smem + (RS ? G * 4 * C::FSF : 2 * G * FS);  // G x [N][NQ] volume
   // element records of groups k .. k + 3 (prefetched three groups ahead, slot k % 4)
@@ -573,7 +577,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     if constexpr (RS) {  // this group's values arrive (issued one iteration ago); the next group's leave
 #pragma unroll
       for (int s = 0; s < 6; ++s) rw[s] = nxt[s];
-      if constexpr (COLOR == 1) {
+      if constexpr (COLOR == 1) {  // (merged schedule: behind the barrier that publishes the wave check)
 #pragma unroll
         for (int s = 0; s < 6; ++s) {
           if constexpr (C::RSP1) prev[s] = nprv[s];
@@ -624,6 +628,12 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     }
     __syncthreads();  // staged faces (and their update) visible to the whole CTA
     // colour-0 partials of the shared faces at q: issued now, consumed at the emits
+    if constexpr (RS && COLOR == 2) {
+      if (col == 1) {
+#pragma unroll
+        for (int s = 0; s < 6; ++s) prev[s] = (on && (shared >> s & 1u)) ? __ldcg(a.r + off[s]) : 0.0;
+      }
+    }
     if (!RS && col == 1 && on) {
       const double* sP = sP0 + buf * G * FS + (act ? e : 0) * FS + q;
 #pragma unroll
@@ -634,7 +644,9 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     // ua = alpha_d u, ur = u
     auto emit = [&](int s, double gval, double ua, double ur) {
       const bool sh = shared >> s & 1u;
-      double val = GONLY ? gval : ((s & 1) ? gcc1 : gcc0) * ua - gval;
+      // explicit roundings: the same bits whichever pass shape (deferred x emits, merged schedule)
+      // the compiler sees around this expression
+      double val = GONLY ? gval : __fma_rn((s & 1) ? gcc1 : gcc0, ua, -gval);
       if (col == 1 && sh) val = prev[s] + val;
       if (CG && (col == 1 || !sh)) {  // final value of w here: Dirichlet row -> 0, <p, w>
         if (kinds[s] == HDGB_DIRICHLET) val = 0.0;
@@ -644,7 +656,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     };
     double gx0 = 0.0, gx1 = 0.0;
     if (FOLD && on) {  // phase 1, folded: x-line of (a2, a3) = (qa, qb), a1 = perm[j] in class order
-      const double x0 = al1 * rw[0], x1 = al1 * rw[1];
+      const double x0 = __dmul_rn(al1, rw[0]), x1 = __dmul_rn(al1, rw[1]);
       const double xs = x0 + x1, xd = x0 - x1;
       const double by = al2 * b0a, bz = al3 * b0b;
       const double base = DZT ? 0.0 : a.lam * al0 + al2 * lama + al3 * lamb;
@@ -661,17 +673,17 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
         if (a1 < NE) ex = fma(K.B0[a1], U, ex);
         else ox = fma(K.B0[a1], U, ox);
       }
-      if constexpr (RS && COLOR == 1) {  // x faces emitted after phase 2: the partials loaded at the top get a whole group to arrive
-        gx0 = al1 * (ex + ox);
-        gx1 = al1 * (ex - ox);
+      if constexpr (RS && COLOR >= 1) {  // x faces emitted after phase 2: the partials loaded at the top get a whole group to arrive
+        gx0 = __dmul_rn(al1, ex + ox);
+        gx1 = __dmul_rn(al1, ex - ox);
       } else {
-        emit(0, al1 * (ex + ox), x0, rw[0]);
-        emit(1, al1 * (ex - ox), x1, rw[1]);
+        emit(0, __dmul_rn(al1, ex + ox), x0, rw[0]);
+        emit(1, __dmul_rn(al1, ex - ox), x1, rw[1]);
       }
     }
     if (!FOLD && on) {  // phase 1: x-line of (a2, a3) = (qa, qb)
       const double xr0 = fb[0][q], xr1 = fb[1][q];
-      const double x0 = al1 * xr0, x1 = al1 * xr1;
+      const double x0 = __dmul_rn(al1, xr0), x1 = __dmul_rn(al1, xr1);
       const double by0 = al2 * b0a, by1 = al2 * b1a, bz0 = al3 * b0b, bz1 = al3 * b1b;
       const double base = DZT ? 0.0 : a.lam * al0 + al2 * lama + al3 * lamb;
       double ax0 = 0.0, ax1 = 0.0;
@@ -692,8 +704,8 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
         ax0 = fma(K.B0[a1], U, ax0);
         ax1 = fma(K.B1[a1], U, ax1);
       }
-      emit(0, al1 * ax0, x0, xr0);
-      emit(1, al1 * ax1, x1, xr1);
+      emit(0, __dmul_rn(al1, ax0), x0, xr0);
+      emit(1, __dmul_rn(al1, ax1), x1, xr1);
     }
     __syncthreads();
     if (on) {  // phase 2: y faces at (a1, a3) = (qa, qb), z faces at (a1, a2) = (qa, qb)
@@ -729,14 +741,14 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       }
       const double yr0 = FOLD ? rw[2] : fb[2][q], yr1 = FOLD ? rw[3] : fb[3][q];
       const double zr0 = FOLD ? rw[4] : fb[4][q], zr1 = FOLD ? rw[5] : fb[5][q];
-      if constexpr (FOLD && RS && COLOR == 1) {
-        emit(0, gx0, al1 * rw[0], rw[0]);
-        emit(1, gx1, al1 * rw[1], rw[1]);
+      if constexpr (FOLD && RS && COLOR >= 1) {
+        emit(0, gx0, __dmul_rn(al1, rw[0]), rw[0]);
+        emit(1, gx1, __dmul_rn(al1, rw[1]), rw[1]);
       }
-      emit(2, al2 * ay0, al2 * yr0, yr0);
-      emit(3, al2 * ay1, al2 * yr1, yr1);
-      emit(4, al3 * az0, al3 * zr0, zr0);
-      emit(5, al3 * az1, al3 * zr1, zr1);
+      emit(2, __dmul_rn(al2, ay0), __dmul_rn(al2, yr0), yr0);
+      emit(3, __dmul_rn(al2, ay1), __dmul_rn(al2, yr1), yr1);
+      emit(4, __dmul_rn(al3, az0), __dmul_rn(al3, zr0), zr0);
+      emit(5, __dmul_rn(al3, az1), __dmul_rn(al3, zr1), zr1);
     }
     // the staging buffer and volume of this group are reused by the next groups behind the next
     // iteration's first barrier (its record slot three groups later); only the merged
@@ -821,7 +833,7 @@ static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
     if (c->efold) return launch_passV<N, MODE | 16, COLOR>(c, a, t0, t1, s);
   }
   using Cf = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, FOLD, (MODE & 5) == 1>;
-  constexpr int SMD = (Cf::RS && COLOR != 2) ? Cf::smem_doubles_rs()
+  constexpr int SMD = Cf::RS ? Cf::smem_doubles_rs()
                      : (Cf::PREV && COLOR == 1) ? Cf::smem_doubles_prev(FOLD)
                      : (FOLD ? Cf::smem_doubles_fold() : Cf::smem_doubles((MODE & 9) == 9 && COLOR == 0));
   static_assert(sizeof(double) * SMD <= 227 * 1024, "element kernel shared memory exceeds 227 KB");
