@@ -227,6 +227,22 @@ struct OpVCfg {
 #ifndef HDGB_OPV_RSP
 #define HDGB_OPV_RSP 2
 #endif
+  // 3 = loaded behind the phase barrier (not live during phase 1)
+#ifdef HDGB_OPV_LATE
+  static constexpr bool LATE = HDGB_OPV_LATE;
+#else
+  // measured (config-3 sweep, p = 3..16): partials loaded behind the phase barrier and the
+  // record re-read there win at N = 9, 12, 13, 15 (p = 8 transformed apply 224 -> 210 us,
+  // transformed PCG 532 -> 514; p = 14 343 -> 314 us, 762 -> 699 us/iter) and lose 2-10 % elsewhere
+  static constexpr bool LATE = N == 9 || N == 12 || N == 13 || N == 15;
+#endif
+  static constexpr bool RSP3 = HDGB_OPV_RSP == 3 || LATE;
+  // RS: face offsets / kinds re-read from the record behind the phase barrier instead of kept
+  // live through phase 1
+#ifndef HDGB_OPV_REREC
+#define HDGB_OPV_REREC 0
+#endif
+  static constexpr bool REREC = HDGB_OPV_REREC || LATE;
   static constexpr bool RSP1 = HDGB_OPV_RSP == 1;  // measured: 2 is 1-14 % faster for p = 3..11 except p = 7 (4 % slower)
   static constexpr int ZOFF_RS = (G * (4 * FSF + VS) + (DZS ? N * NQ : 0) + 1) / 2 * 2;
   __host__ __device__ static constexpr int smem_doubles_rs() { return PU ? ZOFF_RS + 4 * G * FS : G * (4 * FSF + VS) + (DZS ? N * NQ : 0); }
@@ -340,9 +356,12 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   constexpr bool RS = C::RS;  // faces (and colour-0 partials) staged in registers
   double* sF0 = smem;              // 2 x G x [6][FSTR] staged faces (RS: G x [4][FSF] folded faces)
   double* sU = smem + (RS ? G * 4 * C::FSF : 2 * G * FS);  // G x [N][NQ] volume
-  // element records of groups k .. k + 3 (prefetched three groups ahead, slot k % 4)
-  __shared__ ERec sRec[4][G];
-  __shared__ __align__(16) double sAl[4][G][4];  // non-uniform: alpha0..3
+  // element records of groups k .. k + 3 (prefetched three groups ahead, slot k % 8)
+  // (8 slots, fetched three groups ahead: a slot is rewritten five groups after its record,
+  // so a thread may re-read record k behind the phase barrier while others fetch group k + 4's)
+  constexpr int RSL = 8;
+  __shared__ ERec sRec[RSL][G];
+  __shared__ __align__(16) double sAl[RSL][G][4];  // non-uniform: alpha0..3
   const Geo& g = a.g;
   const int tid = threadIdx.x;
   const int e = tid / NQ, q = tid - (tid / NQ) * NQ;
@@ -388,7 +407,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   // groups past the end of this CTA's work get a zero (invalid) record
   constexpr int RW = UNI ? 4 : 8;  // 8-byte words per element: record (+ alpha0..3)
   auto fetch = [&](int64_t k, bool async) {
-    const int sl = (int)(k & 3);
+    const int sl = (int)(k & (RSL - 1));
     for (int c = tid; c < G * RW; c += C::NT) {
       const int ee = c / RW, part = c - ee * RW;
       int col;
@@ -488,7 +507,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   // new loads share (ncu: one DADD with 32 % of the stall samples)
   auto rs_issue = [&](int64_t kk, unsigned dep) {
     if constexpr (RS) {
-      const uint4* R = reinterpret_cast<const uint4*>(&sRec[kk & 3][act ? e : 0]);
+      const uint4* R = reinterpret_cast<const uint4*>(&sRec[kk & (RSL - 1)][act ? e : 0]);
       const uint4 w0 = R[0], w1 = R[1];
       const uint32_t o[6] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y};
       const bool ok = act && kk < nslots && (w1.z & 1u);
@@ -517,10 +536,10 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   for (int64_t k = 0; k < nslots; ++k) {
     const int buf = (int)(k & 1);
     // RS: no barrier here (the folded faces of group k - 1 were last read before its phase
-    // barrier, record k + 1 was published by the barriers of iteration k - 1, and slot
-    // (k + 3) & 3 held record k - 1, last read at the top of iteration k - 1)
+    // barrier, record k + 1 was published by the barriers of iteration k - 1, and the slot of
+    // record k + 3 last held record k - 5)
     if (!RS) __syncthreads();
-    if ((!RS || PUPD) && k + 1 < nslots) stage(sRec[(k + 1) & 3], sF0 + (buf ^ 1) * G * FS, buf ^ 1);
+    if ((!RS || PUPD) && k + 1 < nslots) stage(sRec[(k + 1) & (RSL - 1)], sF0 + (buf ^ 1) * G * FS, buf ^ 1);
     if (k + 3 < nslots) fetch(k + 3, true);
     cp_async_commit();
     asm volatile("cp.async.wait_group 1;\n" ::);
@@ -536,7 +555,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       verified = need > verified ? need : verified;
     }
     // element geometry into registers once (record k was published two barriers ago)
-    const uint4* Iw = reinterpret_cast<const uint4*>(&sRec[k & 3][act ? e : 0]);  // two 128-bit reads
+    const uint4* Iw = reinterpret_cast<const uint4*>(&sRec[k & (RSL - 1)][act ? e : 0]);  // two 128-bit reads
     const uint4 i0 = Iw[0], i1 = Iw[1];
     const uint32_t roff[6] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y};
     const uint32_t flags = i1.z;
@@ -548,8 +567,8 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       off[s2] = roff[s2] + (unsigned)q;
       kinds[s2] = CG ? (int)(flags >> (8 + 3 * s2) & 7u) : 0;
     }
-    const unsigned shared = flags >> 1 & 63u;
-    const double* alp = UNI ? a.al_u : sAl[k & 3][act ? e : 0];
+    unsigned shared = flags >> 1 & 63u;
+    const double* alp = UNI ? a.al_u : sAl[k & (RSL - 1)][act ? e : 0];
     const double al0 = alp[0], al1 = alp[1], al2 = alp[2], al3 = alp[3];
     double* sFw = sF0 + buf * G * FS + (act ? e : 0) * FS;
     double* fb[6];  // face s of the element: fb[s][position]
@@ -581,7 +600,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
 #pragma unroll
         for (int s = 0; s < 6; ++s) {
           if constexpr (C::RSP1) prev[s] = nprv[s];
-          else prev[s] = (on && (shared >> s & 1u)) ? __ldcg(a.r + off[s]) : 0.0;
+          else if constexpr (!C::RSP3) prev[s] = (on && (shared >> s & 1u)) ? __ldcg(a.r + off[s]) : 0.0;
         }
       }
       unsigned dep = 0;
@@ -673,7 +692,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
         if (a1 < NE) ex = fma(K.B0[a1], U, ex);
         else ox = fma(K.B0[a1], U, ox);
       }
-      if constexpr (RS && COLOR >= 1) {  // x faces emitted after phase 2: the partials loaded at the top get a whole group to arrive
+      if constexpr (RS && (COLOR >= 1 || C::REREC)) {  // x faces emitted after phase 2: the partials loaded at the top get a whole group to arrive
         gx0 = __dmul_rn(al1, ex + ox);
         gx1 = __dmul_rn(al1, ex - ox);
       } else {
@@ -708,6 +727,20 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       emit(1, __dmul_rn(al1, ax1), x1, xr1);
     }
     __syncthreads();
+    if constexpr (RS && C::REREC) {  // offsets / kinds were dead through phase 1
+      const uint4 j0 = Iw[0], j1 = Iw[1];
+      const uint32_t ro[6] = {j0.x, j0.y, j0.z, j0.w, j1.x, j1.y};
+#pragma unroll
+      for (int s2 = 0; s2 < 6; ++s2) {
+        off[s2] = ro[s2] + (unsigned)q;
+        kinds[s2] = CG ? (int)(j1.z >> (8 + 3 * s2) & 7u) : 0;
+      }
+      shared = j1.z >> 1 & 63u;
+    }
+    if constexpr (RS && COLOR == 1 && C::RSP3) {
+#pragma unroll
+      for (int s = 0; s < 6; ++s) prev[s] = (on && (shared >> s & 1u)) ? __ldcg(a.r + off[s]) : 0.0;
+    }
     if (on) {  // phase 2: y faces at (a1, a3) = (qa, qb), z faces at (a1, a2) = (qa, qb)
       const double* ycol = vU + qa * C::S1 + qb * C::S3;  // over a2
       const double* zrow = vU + qa * C::S1 + qb * C::S2;  // over a3
@@ -741,7 +774,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       }
       const double yr0 = FOLD ? rw[2] : fb[2][q], yr1 = FOLD ? rw[3] : fb[3][q];
       const double zr0 = FOLD ? rw[4] : fb[4][q], zr1 = FOLD ? rw[5] : fb[5][q];
-      if constexpr (FOLD && RS && COLOR >= 1) {
+      if constexpr (FOLD && RS && (COLOR >= 1 || C::REREC)) {
         emit(0, gx0, __dmul_rn(al1, rw[0]), rw[0]);
         emit(1, gx1, __dmul_rn(al1, rw[1]), rw[1]);
       }
