@@ -146,7 +146,8 @@ struct OpVCfg {
   // apply p = 12 265 -> 239 us, p = 14 324 -> 310 us, transformed PCG 720 -> 651 and 793 -> 763
   // us/iter; N = 14 mixed (apply 265 vs 275, transformed PCG 804 vs 770), N = 16 keeps the
   // bulk copies: 263 vs 277 us)
-  static constexpr bool TMA = N >= HDGB_OPV_TMA_NMIN && N <= HDGB_OPV_TMA_NMAX && !(N & 1);
+  // (N = 14: bulk copies only outside the transformed CG passes: transformed PCG 804 -> 770 us/iter)
+  static constexpr bool TMA = N >= HDGB_OPV_TMA_NMIN && N <= HDGB_OPV_TMA_NMAX && !(N & 1) && !(N == 14 && (PU || CGT));
   // folded kernel: the even- and odd-class folded faces (sum / difference of the two sides) are
   // read side by side by lanes of either class; slots FSF doubles apart with FSF mod 16 in
   // [N, 16 - N] (N <= 8: disjoint banks) or = N (N = 9..15: nearly so) avoid bank conflicts

@@ -52,6 +52,23 @@ def main():
             chk = float(r.double().abs().sum().item())
             print(f"p={p} m={m} variant={variant} us={t:.1f} min={min(ts):.1f} frac16={16 * N / t / 1e3 / hbm:.3f} "
                   f"sum|r|={chk:.12e}", flush=True)
+        if os.environ.get("HDGB_PROBE_PREC"):
+            for kind, name in ((1, "block_prec"), (3, "eigen_diag_prec")):
+                for _ in range(3):
+                    dc.prec(u, kind, out=r)
+                ts = []
+                for _ in range(10):
+                    flush.zero_()
+                    a = torch.cuda.Event(enable_timing=True)
+                    b = torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    dc.prec(u, kind, out=r)
+                    b.record(stream)
+                    b.synchronize()
+                    ts.append(a.elapsed_time(b) * 1e3)
+                t = statistics.median(ts)
+                print(f"p={p} {name} us={t:.1f} frac16={16 * N / t / 1e3 / hbm:.3f} sum|z|={float(r.abs().sum().item()):.12e}",
+                      flush=True)
         if os.environ.get("HDGB_PROBE_PCG", "1") != "0":
             F = r.clone()
             F.copy_(u)
