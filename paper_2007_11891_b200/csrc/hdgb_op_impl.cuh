@@ -244,9 +244,14 @@ struct OpVCfg {
 #define HDGB_OPV_REREC 0
 #endif
   static constexpr bool REREC = HDGB_OPV_REREC || LATE;
+  // 0 = staged through cp.async slots one group ahead like the pre-RS kernel (no registers, full
+  // prefetch distance, 12 more shared accesses per thread and group)
+  static constexpr bool RSP0 = HDGB_OPV_RSP == 0 && !LATE;
   static constexpr bool RSP1 = HDGB_OPV_RSP == 1;  // measured: 2 is 1-14 % faster for p = 3..11 except p = 7 (4 % slower)
   static constexpr int ZOFF_RS = (G * (4 * FSF + VS) + (DZS ? N * NQ : 0) + 1) / 2 * 2;
   __host__ __device__ static constexpr int smem_doubles_rs() { return PU ? ZOFF_RS + 4 * G * FS : G * (4 * FSF + VS) + (DZS ? N * NQ : 0); }
+  static constexpr int POFF_RS = ((PU ? ZOFF_RS + 4 * G * FS : G * (4 * FSF + VS) + (DZS ? N * NQ : 0)) + 1) / 2 * 2;
+  __host__ __device__ static constexpr int smem_doubles_rs_prev() { return POFF_RS + 2 * G * FS; }
   __host__ __device__ static constexpr int smem_doubles_prev(bool fold) { return (fold ? smem_doubles_fold() : smem_doubles(PU)) + 2 * G * FS; }
   __host__ __device__ static constexpr int POFF(bool fold) { return fold ? smem_doubles_fold() : smem_doubles(PU); }
 };
@@ -424,8 +429,8 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       else *dst = __ldg(src);
     }
   };
-  constexpr bool PREV = C::PREV && COLOR == 1 && !RS;  // colour-0 partials staged with the faces
-  double* sP0 = smem + C::POFF(FOLD);            // PREV: 2 x G x [6][FSTR] staged partials
+  constexpr bool PREV = COLOR == 1 && (RS ? C::RSP0 : C::PREV);  // colour-0 partials staged with the faces
+  double* sP0 = smem + (RS ? C::POFF_RS : C::POFF(FOLD));  // PREV: 2 x G x [6][FSTR] staged partials
   double* sZ0 = smem + (RS ? C::ZOFF_RS : C::ZOFF);  // PUPD: 2 x G x [6][FSTR] staged z
   double* sX0 = sZ0 + 2 * G * FS;    // PUPD: 2 x G x [6][FSTR] staged x
   if (TMA && tid == 0) {
@@ -532,7 +537,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   __syncthreads();
   if (!CG) pdl_wait();  // u and r come from earlier kernels
   if (RS) rs_issue(0, 0u);
-  if ((!RS || PUPD) && nslots > 0) stage(sRec[0], sF0, 0);
+  if ((!RS || PUPD || PREV) && nslots > 0) stage(sRec[0], sF0, 0);
   cp_async_commit();
   for (int64_t k = 0; k < nslots; ++k) {
     const int buf = (int)(k & 1);
@@ -540,7 +545,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
     // barrier, record k + 1 was published by the barriers of iteration k - 1, and the slot of
     // record k + 3 last held record k - 5)
     if (!RS) __syncthreads();
-    if ((!RS || PUPD) && k + 1 < nslots) stage(sRec[(k + 1) & (RSL - 1)], sF0 + (buf ^ 1) * G * FS, buf ^ 1);
+    if ((!RS || PUPD || PREV) && k + 1 < nslots) stage(sRec[(k + 1) & (RSL - 1)], sF0 + (buf ^ 1) * G * FS, buf ^ 1);
     if (k + 3 < nslots) fetch(k + 3, true);
     cp_async_commit();
     asm volatile("cp.async.wait_group 1;\n" ::);
@@ -601,7 +606,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
 #pragma unroll
         for (int s = 0; s < 6; ++s) {
           if constexpr (C::RSP1) prev[s] = nprv[s];
-          else if constexpr (!C::RSP3) prev[s] = (on && (shared >> s & 1u)) ? __ldcg(a.r + off[s]) : 0.0;
+          else if constexpr (!C::RSP3 && !C::RSP0) prev[s] = (on && (shared >> s & 1u)) ? __ldcg(a.r + off[s]) : 0.0;
         }
       }
       unsigned dep = 0;
@@ -654,7 +659,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
         for (int s = 0; s < 6; ++s) prev[s] = (on && (shared >> s & 1u)) ? __ldcg(a.r + off[s]) : 0.0;
       }
     }
-    if (!RS && col == 1 && on) {
+    if ((!RS || PREV) && col == 1 && on) {
       const double* sP = sP0 + buf * G * FS + (act ? e : 0) * FS + q;
 #pragma unroll
       for (int s = 0; s < 6; ++s)
@@ -867,7 +872,7 @@ static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
     if (c->efold) return launch_passV<N, MODE | 16, COLOR>(c, a, t0, t1, s);
   }
   using Cf = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, FOLD, (MODE & 5) == 1>;
-  constexpr int SMD = Cf::RS ? Cf::smem_doubles_rs()
+  constexpr int SMD = Cf::RS ? ((COLOR == 1 && Cf::RSP0) ? Cf::smem_doubles_rs_prev() : Cf::smem_doubles_rs())
                      : (Cf::PREV && COLOR == 1) ? Cf::smem_doubles_prev(FOLD)
                      : (FOLD ? Cf::smem_doubles_fold() : Cf::smem_doubles((MODE & 9) == 9 && COLOR == 0));
   static_assert(sizeof(double) * SMD <= 227 * 1024, "element kernel shared memory exceeds 227 KB");

@@ -76,8 +76,26 @@ def report(rows, hdr, launch, nl):
     if ci is None:
         print("columns:", hdr)
         return
+    ex = lambda name: hdr.index(name) if name in hdr else None
+    wi, ii, ei = ex("L1 Wavefronts Shared"), ex("L1 Wavefronts Shared Ideal"), ex("Instructions Executed")
+    ops = {}
+    if wi is not None:
+        for r in rows:
+            w = float(r[wi] or 0)
+            if w <= 0:
+                continue
+            toks = r[si].replace("@P0", "").replace("@!P0", "").split()
+            op = next((t for t in toks if t[:3] in ("LDS", "STS", "LDG", "ATO", "RED")), toks[0] if toks else "?")
+            o = ops.setdefault(op, [0.0, 0.0, 0.0])
+            o[0] += w
+            o[1] += float(r[ii] or 0)
+            o[2] += float(r[ei] or 0)
     tot = sum(float(r[ci] or 0) for r in rows)
     print(f"--- launch {launch}: stall samples {tot:.0f}")
+    if ops:
+        print(f"--- launch {launch}: shared wavefronts by opcode")
+        for op, (w, i, n) in sorted(ops.items(), key=lambda kv: -kv[1][0]):
+            print(f"  {op:<26} wavefronts {w:>10.0f} ideal {i:>10.0f} inst {n:>10.0f}")
     best = sorted(rows, key=lambda r: -float(r[ci] or 0))[:nl]
     for r in best:
         ls = col("stall_long_sb"); ss = col("stall_short_sb"); bs = col("stall_barrier")
