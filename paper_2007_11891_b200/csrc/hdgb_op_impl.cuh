@@ -223,31 +223,28 @@ struct OpVCfg {
 #endif
   // (with the fused direction update, PU: p in registers, z and x still through cp.async slots)
   static constexpr bool RS = HDGB_OPV_RS && FO && !TMA && (!PU || HDGB_OPV_RSPU);
-  // colour-0 partials under RS: 1 = in registers one group ahead, 2 = loaded at the top of their
-  // own group (consumed at the emits)
-#ifndef HDGB_OPV_RSP
-#define HDGB_OPV_RSP 2
-#endif
-  // 3 = loaded behind the phase barrier (not live during phase 1)
-#ifdef HDGB_OPV_LATE
-  static constexpr bool LATE = HDGB_OPV_LATE;
+  // Colour-0 partials of colour pass 1 under RS (RSP): 0 = through cp.async slots one group
+  // ahead like the pre-RS kernel (no registers, full prefetch distance, 12 more shared accesses
+  // per thread and group), 1 = in registers one group ahead (spills at 128 registers), 2 =
+  // loaded at the top of their own group, 3 = loaded behind the phase barrier (not live during
+  // phase 1, but the first emit waits for them: ncu, 28 % of the stall samples at N = 9).
+  // REREC: face offsets / kinds re-read from the record behind the phase barrier instead of
+  // kept live through phase 1 (all x emits then follow phase 2).  Measured on the config-3
+  // sweep, transformed apply / transformed PCG per iteration, us:
+  //   N = 9:  RSP 2 224 / 532, RSP 3 + REREC 210 / 514, RSP 0 + REREC 200 / 501
+  //   N = 13: RSP 2 239 / 638, RSP 3 + REREC 232 / 616;  N = 15: 343 / 762 -> 314 / 699
+  //   N = 12: 234 / 583 -> 234 / 548;  every other N: RSP 2 without REREC is 2-10 % faster
+#ifdef HDGB_OPV_RSP
+  static constexpr int RSP = HDGB_OPV_RSP;
 #else
-  // measured (config-3 sweep, p = 3..16): partials loaded behind the phase barrier and the
-  // record re-read there win at N = 9, 12, 13, 15 (p = 8 transformed apply 224 -> 210 us,
-  // transformed PCG 532 -> 514; p = 14 343 -> 314 us, 762 -> 699 us/iter) and lose 2-10 % elsewhere
-  static constexpr bool LATE = N == 9 || N == 12 || N == 13 || N == 15;
+  static constexpr int RSP = N == 9 ? 0 : ((N == 12 || N == 13 || N == 15) ? 3 : 2);
 #endif
-  static constexpr bool RSP3 = HDGB_OPV_RSP == 3 || LATE;
-  // RS: face offsets / kinds re-read from the record behind the phase barrier instead of kept
-  // live through phase 1
-#ifndef HDGB_OPV_REREC
-#define HDGB_OPV_REREC 0
+#ifdef HDGB_OPV_REREC
+  static constexpr bool REREC = HDGB_OPV_REREC;
+#else
+  static constexpr bool REREC = N == 9 || N == 12 || N == 13 || N == 15;
 #endif
-  static constexpr bool REREC = HDGB_OPV_REREC || LATE;
-  // 0 = staged through cp.async slots one group ahead like the pre-RS kernel (no registers, full
-  // prefetch distance, 12 more shared accesses per thread and group)
-  static constexpr bool RSP0 = HDGB_OPV_RSP == 0 && !LATE;
-  static constexpr bool RSP1 = HDGB_OPV_RSP == 1;  // measured: 2 is 1-14 % faster for p = 3..11 except p = 7 (4 % slower)
+  static constexpr bool RSP0 = RSP == 0, RSP1 = RSP == 1, RSP3 = RSP == 3;
   static constexpr int ZOFF_RS = (G * (4 * FSF + VS) + (DZS ? N * NQ : 0) + 1) / 2 * 2;
   __host__ __device__ static constexpr int smem_doubles_rs() { return PU ? ZOFF_RS + 4 * G * FS : G * (4 * FSF + VS) + (DZS ? N * NQ : 0); }
   static constexpr int POFF_RS = ((PU ? ZOFF_RS + 4 * G * FS : G * (4 * FSF + VS) + (DZS ? N * NQ : 0)) + 1) / 2 * 2;
