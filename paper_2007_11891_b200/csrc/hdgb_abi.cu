@@ -313,9 +313,9 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
     // default per degree (config-3 sweep, transformed apply at ~2e7 unknowns): folded faster at
     // p = 3 (160 vs 174 us), 8 (246 vs 252), 12 (275 vs 288), 16 (374 vs 414); slower at p = 2
     // (296 vs 202) and p = 4 (236 vs 200); HDGB_EFOLD=1 forces it on, =0 off
-    // (with register-staged faces the folded kernel also wins at p = 2: 194 -> 183 us; p = 4
-    // stays unfolded: 196 vs 222 us)
-    const bool efdef = N == 3 || N == 4 || N >= 6;
+    // (with register-staged faces: p = 2 folded 183 us, unfolded 173 us; p = 4 unfolded 185 vs
+    // folded 222 us; p = 3, 5, 8 folded 142 / 167 / 200 vs unfolded 141 / 179 / 216 us)
+    const bool efdef = N == 4 || N >= 6;
     c->efold = ok && neven == (N + 1) / 2 && dev <= 2.5e-12 * bmx && !(ef && atoi(ef) == 0) &&
                (efdef || (ef && atoi(ef) == 1));
     if (c->efold) {

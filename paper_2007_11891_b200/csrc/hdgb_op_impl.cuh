@@ -222,7 +222,14 @@ struct OpVCfg {
 #define HDGB_OPV_RSPU 1
 #endif
   // (with the fused direction update, PU: p in registers, z and x still through cp.async slots)
-  static constexpr bool RS = HDGB_OPV_RS && FO && !TMA && (!PU || HDGB_OPV_RSPU);
+  // (unfolded kernel, N = 2, 3 and 5 by default: the raw y / z faces take the place of the folded
+  // ones; not in the transformed CG passes: p = 4 transformed apply 194 -> 185 us but transformed
+  // PCG 528 -> 579 us/iter with them)
+#ifndef HDGB_OPV_RSU
+#define HDGB_OPV_RSU 1
+#endif
+  static constexpr bool RS = HDGB_OPV_RS && (FO || (HDGB_OPV_RSU && !PU && !CGT)) && !TMA && (!PU || HDGB_OPV_RSPU);
+  static constexpr int RSTR = FO ? FSF : NQ;  // RS: slot stride of the four y / z faces of an element
   // Colour-0 partials of colour pass 1 under RS (RSP): 0 = through cp.async slots one group
   // ahead like the pre-RS kernel (no registers, full prefetch distance, 12 more shared accesses
   // per thread and group), 1 = in registers one group ahead (spills at 128 registers), 2 =
@@ -245,9 +252,9 @@ struct OpVCfg {
   static constexpr bool REREC = N == 9 || N == 12 || N == 13 || N == 15;
 #endif
   static constexpr bool RSP0 = RSP == 0, RSP1 = RSP == 1, RSP3 = RSP == 3;
-  static constexpr int ZOFF_RS = (G * (4 * FSF + VS) + (DZS ? N * NQ : 0) + 1) / 2 * 2;
-  __host__ __device__ static constexpr int smem_doubles_rs() { return PU ? ZOFF_RS + 4 * G * FS : G * (4 * FSF + VS) + (DZS ? N * NQ : 0); }
-  static constexpr int POFF_RS = ((PU ? ZOFF_RS + 4 * G * FS : G * (4 * FSF + VS) + (DZS ? N * NQ : 0)) + 1) / 2 * 2;
+  static constexpr int ZOFF_RS = (G * (4 * RSTR + VS) + (DZS ? N * NQ : 0) + 1) / 2 * 2;
+  __host__ __device__ static constexpr int smem_doubles_rs() { return PU ? ZOFF_RS + 4 * G * FS : G * (4 * RSTR + VS) + (DZS ? N * NQ : 0); }
+  static constexpr int POFF_RS = ((PU ? ZOFF_RS + 4 * G * FS : G * (4 * RSTR + VS) + (DZS ? N * NQ : 0)) + 1) / 2 * 2;
   __host__ __device__ static constexpr int smem_doubles_rs_prev() { return POFF_RS + 2 * G * FS; }
   __host__ __device__ static constexpr int smem_doubles_prev(bool fold) { return (fold ? smem_doubles_fold() : smem_doubles(PU)) + 2 * G * FS; }
   __host__ __device__ static constexpr int POFF(bool fold) { return fold ? smem_doubles_fold() : smem_doubles(PU); }
@@ -358,7 +365,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
   __shared__ __align__(8) uint64_t sBar[2];  // TMA: one transaction barrier per staging buffer
   constexpr bool RS = C::RS;  // faces (and colour-0 partials) staged in registers
   double* sF0 = smem;              // 2 x G x [6][FSTR] staged faces (RS: G x [4][FSF] folded faces)
-  double* sU = smem + (RS ? G * 4 * C::FSF : 2 * G * FS);  // G x [N][NQ] volume
+  double* sU = smem + (RS ? G * 4 * C::RSTR : 2 * G * FS);  // G x [N][NQ] volume
   // element records of groups k .. k + 3 (prefetched three groups ahead, slot k % 8)
   // (8 slots, fetched three groups ahead: a slot is rewritten five groups after its record,
   // so a thread may re-read record k behind the phase barrier while others fetch group k + 4's)
@@ -625,6 +632,14 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
         }
       }
     }
+    if constexpr (RS && !FOLD) {  // unfolded: the raw y / z faces (this thread's position) out
+      double* fo = smem + (act ? e : 0) * 4 * C::RSTR;
+#pragma unroll
+      for (int s = 2; s < 6; ++s) {
+        fb[s] = fo + (s - 2) * C::RSTR;
+        if (on) fb[s][q] = rw[s];
+      }
+    }
     // folded faces in permuted order: y (sum / difference of the two sides) [j1][j3], z [j1][j2];
     // phase 1 reads the class of its own a2 (y) and a3 (z)
     const double* ysel = nullptr;
@@ -704,7 +719,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
       }
     }
     if (!FOLD && on) {  // phase 1: x-line of (a2, a3) = (qa, qb)
-      const double xr0 = fb[0][q], xr1 = fb[1][q];
+      const double xr0 = RS ? rw[0] : fb[0][q], xr1 = RS ? rw[1] : fb[1][q];
       const double x0 = __dmul_rn(al1, xr0), x1 = __dmul_rn(al1, xr1);
       const double by0 = al2 * b0a, by1 = al2 * b1a, bz0 = al3 * b0b, bz1 = al3 * b1b;
       const double base = DZT ? 0.0 : a.lam * al0 + al2 * lama + al3 * lamb;
@@ -726,8 +741,13 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
         ax0 = fma(K.B0[a1], U, ax0);
         ax1 = fma(K.B1[a1], U, ax1);
       }
-      emit(0, __dmul_rn(al1, ax0), x0, xr0);
-      emit(1, __dmul_rn(al1, ax1), x1, xr1);
+      if constexpr (RS && (COLOR >= 1 || C::REREC)) {  // like the folded branch: x emits behind phase 2
+        gx0 = __dmul_rn(al1, ax0);
+        gx1 = __dmul_rn(al1, ax1);
+      } else {
+        emit(0, __dmul_rn(al1, ax0), x0, xr0);
+        emit(1, __dmul_rn(al1, ax1), x1, xr1);
+      }
     }
     __syncthreads();
     if constexpr (RS && C::REREC) {  // offsets / kinds were dead through phase 1
@@ -775,9 +795,9 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
           az1 = fma(K.B1[k], vz, az1);
         }
       }
-      const double yr0 = FOLD ? rw[2] : fb[2][q], yr1 = FOLD ? rw[3] : fb[3][q];
-      const double zr0 = FOLD ? rw[4] : fb[4][q], zr1 = FOLD ? rw[5] : fb[5][q];
-      if constexpr (FOLD && RS && (COLOR >= 1 || C::REREC)) {
+      const double yr0 = (FOLD || RS) ? rw[2] : fb[2][q], yr1 = (FOLD || RS) ? rw[3] : fb[3][q];
+      const double zr0 = (FOLD || RS) ? rw[4] : fb[4][q], zr1 = (FOLD || RS) ? rw[5] : fb[5][q];
+      if constexpr (RS && (COLOR >= 1 || C::REREC)) {
         emit(0, gx0, __dmul_rn(al1, rw[0]), rw[0]);
         emit(1, gx1, __dmul_rn(al1, rw[1]), rw[1]);
       }
