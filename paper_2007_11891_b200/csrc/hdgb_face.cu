@@ -203,7 +203,20 @@ struct FxCfg {
 #ifndef HDGB_FXPC_S
 #define HDGB_FXPC_S 0
 #endif
-  static constexpr int S = (FK == FX_TRANSFORM && CG && HDGB_FXT_S) ? HDGB_FXT_S
+  // Large N: ONE stage (the batch is fetched at the top of its own iteration, latency exposed)
+  // fits a third CTA per SM, which hides more than the prefetch did.  Block PCG, us/iter, two
+  // stages -> one: fused update p = 13 836 -> 783, p = 14 958 -> 862; all three PCG kernels
+  // p = 15 1040 -> 858, p = 16 1070 -> 1010 (p = 12 and below: slower)
+#ifndef HDGB_FX_S1U_N
+#define HDGB_FX_S1U_N 14
+#endif
+#ifndef HDGB_FX_S1_N
+#define HDGB_FX_S1_N 16
+#endif
+  static constexpr bool ONE = CG && ((FK == FX_UPDATE && N >= HDGB_FX_S1U_N) ||
+                                     ((FK == FX_TRANSFORM || FK == FX_POST) && N >= HDGB_FX_S1_N));
+  static constexpr int S = ONE ? 1
+                           : (FK == FX_TRANSFORM && CG && HDGB_FXT_S) ? HDGB_FXT_S
                            : (FK == FX_UPDATE && CG && HDGB_FXU_S) ? HDGB_FXU_S
                            : (FK == FX_POST && CG && HDGB_FXPC_S) ? HDGB_FXPC_S
                                                                    : 2;  // ring stages per group
@@ -256,7 +269,7 @@ struct FxCfg {
 #endif
   // N <= 11: 4 CTAs/SM for every kind (block PCG p = 4 744 -> 722, p = 8 772 -> 761, p = 10 789 -> 779 us/iter)
   static constexpr int MINB = N <= HDGB_FX_MINB4_N ? 4
-                              : ((FK == FX_POST && !CG && OPS == 2) || (FK == FX_PREC && N >= 8)) ? 3
+                              : (ONE || (FK == FX_POST && !CG && OPS == 2) || (FK == FX_PREC && N >= 8)) ? 3
                               : (FK == FX_UPDATE ? HDGB_FXU_MINB
                                                  : (FK == FX_TRANSFORM && CG ? HDGB_FXT_MINB
                                                                              : (FK == FX_POST && CG ? HDGB_FXPC_MINB : 2)));
