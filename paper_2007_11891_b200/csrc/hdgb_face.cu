@@ -213,8 +213,14 @@ struct FxCfg {
 #ifndef HDGB_FX_S1_N
 #define HDGB_FX_S1_N 16
 #endif
-  static constexpr bool ONE = CG && ((FK == FX_UPDATE && N >= HDGB_FX_S1U_N) ||
-                                     ((FK == FX_TRANSFORM || FK == FX_POST) && N >= HDGB_FX_S1_N));
+// (one stage for the standalone kernels too, N >= 13: plain apply 8-28 % slower, block
+// preconditioner mixed (p = 14 167 -> 144 us, p = 12 128 -> 142 us): off)
+#ifndef HDGB_FX_S1A_N
+#define HDGB_FX_S1A_N 99
+#endif
+  static constexpr bool ONE = (CG && ((FK == FX_UPDATE && N >= HDGB_FX_S1U_N) ||
+                                      ((FK == FX_TRANSFORM || FK == FX_POST) && N >= HDGB_FX_S1_N))) ||
+                              (!CG && N >= HDGB_FX_S1A_N);
   static constexpr int S = ONE ? 1
                            : (FK == FX_TRANSFORM && CG && HDGB_FXT_S) ? HDGB_FXT_S
                            : (FK == FX_UPDATE && CG && HDGB_FXU_S) ? HDGB_FXU_S
