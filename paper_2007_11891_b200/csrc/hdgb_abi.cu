@@ -98,6 +98,7 @@ int hdgb_ctx_create(const hdgb_desc* d, hdgb_ctx** out) {
   c->dev = d->device;
   if (const char* sb = getenv("HDGB_SLAB_MB")) c->slab_bytes = (int64_t)atof(sb) * (1LL << 20);
   if (const char* gc = getenv("HDGB_GRID_CAP")) c->grid_cap = atoll(gc);
+  if (const char* sw = getenv("HDGB_SG_WAVES")) c->sg_waves = atoi(sw);
   // merged colour schedule: was the default at N = 17 until the element kernel staged its faces
   // in registers (separate passes only): p = 16 transformed apply 343 -> 323 us, transformed PCG
   // 821 -> 688 us/iter unmerged

@@ -346,6 +346,7 @@ struct hdgb_ctx {
   // kernels, so every CTA walks several element groups / face batches through its staging
   // ring; 0 = the resident grid
   int64_t grid_cap = 0;
+  int sg_waves = 6;  // element kernel: small-grid launch shape below this many groups per CTA (0: never)
   // merged colour schedule of the element kernel (both passes in one launch, L2-ordered):
   // per-wave arrival counters (npairs + 2 words, zero between launches).  Measured on config 3:
   // DRAM traffic of the pair at p = 8 drops from 732 to 404 MB (algorithmic 324 MB), but the

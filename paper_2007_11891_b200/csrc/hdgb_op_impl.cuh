@@ -98,7 +98,11 @@ __device__ __forceinline__ void elem_alpha(const OpArgs& a, const int* c, double
 // PU: the colour-0 pass with the fused PCG direction update (MODE bits 0 and 3); FO: the
 // parity-folded kernel (MODE bit 4)
 // CGT: the transformed operator in CG mode (Dirichlet rows, <p, w>)
-template <int N, bool PU = false, bool FO = false, bool CGT = false>
+// SG: small-grid shape (MODE bit 5): one warp-rounded element group per CTA, chosen at launch
+// when the default shape would give every CTA fewer than HDGB_OPV_SG_WAVES groups (config 2:
+// 2048 elements per colour pass = 2.3 groups of 3 elements per CTA; the finer shape balances the
+// SMs and shortens the critical path)
+template <int N, bool PU = false, bool FO = false, bool CGT = false, bool SG = false>
 struct OpVCfg {
   static constexpr int NQ = N * N;                      // threads (face positions) per element
 #ifndef HDGB_OPV_THREADS
@@ -118,14 +122,17 @@ struct OpVCfg {
   // (not the fused-update colour-0 pass at N = 13: its staging measured slower
   // in the small shape: transformed PCG p = 12 614 -> 676 us/iter)
   static constexpr bool SMALL = ((N >= HDGB_OPV_SMALL_N0 && N <= HDGB_OPV_SMALL_N1) || N == 8) && !(PU && N == 13);
-  static constexpr int THREADS = SMALL ? 128 : HDGB_OPV_THREADS;
+  static constexpr int THREADS = SG ? (NQ > 32 ? (NQ + 31) / 32 * 32 : 32) : (SMALL ? 128 : HDGB_OPV_THREADS);
   static constexpr int G = NQ >= THREADS ? 1 : THREADS / NQ;  // elements per CTA
   static constexpr int NT = (G * NQ + 31) / 32 * 32;    // threads per CTA
+  // the small-grid shape exists where the default one packs several elements into a CTA
+  static constexpr bool HAS_SG = !SG && !SMALL && (NQ < HDGB_OPV_THREADS ? HDGB_OPV_THREADS / NQ : 1) > 1;
 #ifdef HDGB_OPV_MINB
   static constexpr int MINB = HDGB_OPV_MINB;
 #else
   // register budget (CTAs per SM): measured on the config-3 sweep (p = 2..16)
-  static constexpr int MINB = SMALL ? 4 : (NT > 256 ? 2 : (N <= 5 ? 3 : (N <= 11 ? 2 : 3)));  // N = 6, 7: 2 (p = 5: 216 -> 210 us)
+  static constexpr int MINB = SG ? (512 / NT > 16 ? 16 : 512 / NT)  // 128 registers per thread
+                                 : (SMALL ? 4 : (NT > 256 ? 2 : (N <= 5 ? 3 : (N <= 11 ? 2 : 3))));  // N = 6, 7: 2 (p = 5: 216 -> 210 us)
 #endif
   // staging of the six faces: bulk async copies (TMA unit, one mbarrier per buffer) for
   // N >= HDGB_OPV_TMA_NMIN, per-thread cp.async below.  A face of odd NQ starts on an 8-byte
@@ -334,10 +341,10 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
 // (bulk-copy staging: separate buffer), in slots N (mod 16) doubles apart so lanes of both
 // classes read them without bank conflicts.
 template <int N, int MODE, int COLOR>
-__global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::NT,
-                                  OpVCfg<N, (MODE & 9) == 9 && COLOR == 0>::MINB) opV_kernel(const OpArgs a, int64_t t0, int64_t t1,
+__global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, false, false, (MODE & 32) != 0>::NT,
+                                  OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, false, false, (MODE & 32) != 0>::MINB) opV_kernel(const OpArgs a, int64_t t0, int64_t t1,
                                                           const __grid_constant__ OpVConst<N> K) {
-  using C = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, (MODE & 16) != 0, (MODE & 5) == 1>;
+  using C = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, (MODE & 16) != 0, (MODE & 5) == 1, (MODE & 32) != 0>;
   constexpr int NQ = C::NQ, G = C::G, FS = C::FS, VS = C::VS;
   constexpr bool UNI = !(MODE & 2), CG = MODE & 1, GONLY = MODE & 4, FOLD = MODE & 16;
   constexpr int NE = (N + 1) / 2;  // FOLD: even-class size (j < NE even)
@@ -888,7 +895,7 @@ static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
   if constexpr (!FOLD) {
     if (c->efold) return launch_passV<N, MODE | 16, COLOR>(c, a, t0, t1, s);
   }
-  using Cf = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, FOLD, (MODE & 5) == 1>;
+  using Cf = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, FOLD, (MODE & 5) == 1, (MODE & 32) != 0>;
   constexpr int SMD = Cf::RS ? ((COLOR == 1 && Cf::RSP0) ? Cf::smem_doubles_rs_prev() : Cf::smem_doubles_rs())
                      : (Cf::PREV && COLOR == 1) ? Cf::smem_doubles_prev(FOLD)
                      : (FOLD ? Cf::smem_doubles_fold() : Cf::smem_doubles((MODE & 9) == 9 && COLOR == 0));
@@ -900,6 +907,9 @@ static cudaError_t launch_passV(hdgb_ctx* c, const OpArgs& a, int64_t t0, int64_
   cudaError_t e = resident_grid(kern, Cf::NT, smem, c->dev, cache, &grid);
   if (e != cudaSuccess) return e;
   const int64_t need = (t1 - t0 + Cf::G - 1) / Cf::G;
+  if constexpr (Cf::HAS_SG && !(MODE & 3) && COLOR != 2) {  // plain and transformed applies on uniform grids
+    if (c->sg_waves > 0 && need < (int64_t)c->sg_waves * grid) return launch_passV<N, MODE | 32, COLOR>(c, a, t0, t1, s);
+  }
   grid = cap_grid(c, grid);
   if (grid > need) grid = need;
   if (grid < 1) return cudaSuccess;
