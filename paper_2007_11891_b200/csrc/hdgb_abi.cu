@@ -632,9 +632,11 @@ cudaError_t enqueue_op_half(hdgb_ctx* c, int variant, cudaStream_t s) {
   double* v = c->d_vec;
   cudaError_t e;
   c->pupd_z = v + V_Z * c->vstride;
+  c->pw_dir = variant == HDGB_TRANSFORMED ? 2 : 0;
   if (variant == HDGB_TRANSFORMED && (c->N < HDGB_PUPD_NMIN || c->N > HDGB_PUPD_NMAX)) {
     if ((e = launch_p_update(c, s)) != cudaSuccess) return e;  // p and the deferred x
     c->pupd_z = nullptr;
+    c->pw_dir = 1;
   }
   c->pupd_x = v + V_X * c->vstride;
   e = launch_op(c, variant, MODE_CG, v + V_P * c->vstride, v + V_W * c->vstride, s);
@@ -661,9 +663,11 @@ static cudaError_t enqueue_iteration(hdgb_ctx* c, int variant, int prec, cudaGra
   // transformed: folded into colour pass 0 for 4 <= N <= 16; at N = 3 (small elements, staging
   // dominated) and N = 17 (the z stage halves the resident CTAs) the separate pass measured
   // as fast or faster (p = 2: 601 vs 596, p = 12: 663 vs 677, p = 14: 745 vs 761 us/iter)
+  c->pw_dir = variant == HDGB_TRANSFORMED ? 2 : 0;
   if (variant == HDGB_TRANSFORMED && (c->N < HDGB_PUPD_NMIN || c->N > HDGB_PUPD_NMAX)) {
     if ((e = launch_p_update(c, c->s)) != cudaSuccess) return e;  // p and the deferred x
     c->pupd_z = nullptr;
+    c->pw_dir = 1;
   }
   // x += alpha p (solver.py:313) deferred into the next direction update, which reads p anyway
   // (x_final applies the last one after the loop); the block preconditioner kernel also takes

@@ -51,8 +51,11 @@ __global__ void __launch_bounds__(256) pw_kernel(FaceArgs a, const uint8_t* __re
   }
   const double alpha = FK == PW_UPDATE ? a.st->alpha : 0.0;
   double rr = 0.0, rz = 0.0;
-  const unsigned stride = gridDim.x * 256u * PW_U;
-  for (unsigned base = blockIdx.x * 256u * PW_U + threadIdx.x; base < n; base += stride) {
+  const unsigned chunk = 256u * PW_U, nchunk = (n + chunk - 1) / chunk;
+  // traversal (FaceArgs::dirmode): the CG update starts where the operator's last pass ended
+  const bool rev = FK == PW_UPDATE && (a.dirmode == 1 || (a.dirmode == 2 && (a.st->it & 1)));
+  for (unsigned c = blockIdx.x; c < nchunk; c += gridDim.x) {
+    const unsigned base = (rev ? nchunk - 1 - c : c) * chunk + threadIdx.x;
     double v0[PW_U], v1[PW_U], v2[PW_U], v3[PW_U];
     uint8_t inf[PW_U];
 #pragma unroll
@@ -1173,6 +1176,7 @@ cudaError_t launch_cg_update(hdgb_ctx* c, int kind, cudaStream_t s, cudaGraphCon
   FaceArgs a = base_args(c, kind);
   a.loop = loop;
   a.loop_on = loop_on;
+  a.dirmode = c->pw_dir;
   double* v = c->d_vec;
   a.x = v + V_X * c->vstride;
   a.p = v + V_P * c->vstride;

@@ -135,6 +135,10 @@ struct OpArgs {
   const uint32_t* erec;  // element records [colour][pair][8] (see hdgb_ctx::d_erec)
   const double* eal;     // non-uniform: alpha0..3 per record
   int64_t npairs;
+  // traversal of the element groups per colour pass: 0 forward, 1 backward, 2 backward in odd
+  // PCG iterations, 3 backward in even ones.  Consecutive passes run in opposite directions so a
+  // pass starts on what the previous one touched last (still in L2)
+  int dirmode[2];
   uint32_t* wdone;       // merged colour schedule: per-wave colour-0 arrivals (+ exit ticket)
   int64_t wcount;        //   waves per colour
   int64_t wlag;          //   colour-0 waves ahead of colour-1 wave 0 (placement)
@@ -164,6 +168,7 @@ struct FaceArgs {
   CGState* st;
   cudaGraphConditionalHandle loop;  // PCG graph: the x, r update ends the loop once done
   int loop_on;
+  int dirmode;  // pointwise CG update: traversal 0 forward, 1 backward, 2 backward in odd iterations
   int fold;              // FX_TRANSFORM: A is the context's T (parity-folded products allowed)
 };
 
@@ -310,6 +315,7 @@ struct hdgb_ctx {
   // plain PCG: z slot of the direction update fused into the pre-transform (set around
   // the operator launch of an iteration; null otherwise)
   const double* pupd_z = nullptr;
+  int pw_dir = 0;            // traversal of the pointwise CG update (FaceArgs::dirmode)
   double* pupd_x = nullptr;  // block PCG: x slot of the deferred x update (also selects the fused r update)
   double* d_io = nullptr;         // host-path staging (2 * n_all)
   cudaStream_t s = nullptr;

@@ -273,6 +273,9 @@ struct OpVCfg {
 // permuted eigen index j (even class first, perm[j] = a), B1 the symmetrised B_S[:,0] in the
 // natural index; sig bit a = eigenvector a even; pS1/pS2/pS3/pN/pNQ[j] = perm[j] times the
 // volume strides / N / N^2 (uniform offsets of the permuted loops).
+#ifndef HDGB_OPV_REVERSE1
+#define HDGB_OPV_REVERSE1 1
+#endif
 template <int N>
 struct OpVConst {
   double B0[N], B1[N], Lam[N];
@@ -407,6 +410,11 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, false
   }
 
   const int64_t ngroups = (t1 - t0 + G - 1) / G;
+  bool rev = false;
+  if (HDGB_OPV_REVERSE1 && COLOR != 2) {
+    const int dm = a.dirmode[COLOR == 1 ? 1 : 0];
+    rev = dm == 1 || (CG && dm >= 2 && ((a.st->it & 1) != 0) == (dm == 2));
+  }
   // slot k of this CTA -> (colour, element group)
   const int64_t nslots = COLOR == 2 ? 2 * (int64_t)a.wcount
                                     : ((int64_t)blockIdx.x < ngroups ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0);
@@ -418,6 +426,7 @@ __global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, false
       col = COLOR;
       w = k;
       gi = blockIdx.x + k * (int64_t)gridDim.x;
+      if (rev) gi = ngroups - 1 - gi;  // OpArgs::dirmode
     }
   };
   // record of group k into slot k % 4: 8-byte words, plain (prologue) or cp.async (loop);
@@ -982,6 +991,8 @@ static cudaError_t launch_t(hdgb_ctx* c, const double* u, double* r, cudaStream_
   a.erec = c->d_erec;
   a.eal = c->d_eal;
   a.npairs = c->npairs;
+  a.dirmode[0] = 0;  // colour pass 1 walks the groups backwards: the partials and faces colour
+  a.dirmode[1] = 1;  // pass 0 touched last are the ones still in L2
   // z-slabs of element pairs, sized so two slabs of face data stay L2-resident
   const int64_t hp = (g.n1 + 1) / 2;
   const int64_t per_k = hp * g.n2;  // pairs per z-layer
@@ -992,7 +1003,13 @@ static cudaError_t launch_t(hdgb_ctx* c, const double* u, double* r, cudaStream_
   const int64_t nslab = (g.n3 + layers - 1) / layers;
   cudaError_t e;
   if constexpr (!PLAIN && (MODE & 1)) {
+    if (c->pupd_x && !c->pupd_z) {  // separate direction-update pass (forward) -> colour 0 backward,
+      a.dirmode[0] = 1;              // colour 1 forward, pointwise update backward (hdgb_abi.cu)
+      a.dirmode[1] = 0;
+    }
     if (c->pupd_z && c->pupd_x) {  // transformed PCG: direction update fused into the colour passes (one slab)
+      a.dirmode[0] = 2;  // three passes per iteration: the directions alternate with the iteration
+      a.dirmode[1] = 3;
       a.z = c->pupd_z;
       a.pout = const_cast<double*>(u);
       a.xout = c->pupd_x;
