@@ -233,6 +233,29 @@ def test_fused_pcg_config2_iterations():
     assert relerr(x, xo) < 1e-10
 
 
+@pytest.mark.parametrize("p", [2, 4, 8, 12])
+def test_fused_pcg_is_bitwise_reproducible(p, monkeypatch):
+    """The fused PCG alternates the traversal direction of its passes with the iteration parity
+    (L2 reuse between passes) and reduces in fixed order: two solves of the same system give the
+    same bits and iteration counts, for both pipelines, with a capped grid so every CTA walks
+    several element groups in both directions."""
+    from paper_2007_11891_b200.operator import DeviceContext
+
+    monkeypatch.setenv("HDGB_GRID_CAP", "3")
+    mesh = hb.Mesh((5, 4, 3), (0, 0, 0), (1.25, 1.0, 0.75), ("dirichlet", "neumann", "dirichlet", "dirichlet",
+                                                            "neumann", "dirichlet"))
+    dc = DeviceContext(hb.Basis1D(p, 0.5), mesh, 0.4)
+    F = dc.unpack(_dev(np.random.default_rng(700 + p).uniform(-1, 1, dc.n_unknown)))
+    for variant, kind in ((0, 1), (1, 3)):
+        runs = []
+        for _ in range(2):
+            x = torch.zeros_like(F)
+            it, rel, conv = dc.pcg(variant, kind, F, x, 1e-300, 0.0, 9)  # odd count: both parities
+            runs.append((x.clone(), it, rel))
+        assert runs[0][1] == runs[1][1] == 9
+        assert torch.equal(runs[0][0], runs[1][0]) and runs[0][2] == runs[1][2]
+
+
 # ---------------------------------------------------------------- generic pcg (arbitrary callables)
 def test_pcg_identity_operator():
     F = np.random.default_rng(3).standard_normal(40)
