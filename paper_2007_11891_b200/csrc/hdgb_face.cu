@@ -254,7 +254,16 @@ struct FxCfg {
   static constexpr bool BLOCK = FK == FX_PREC || FK == FX_INIT || FK == FX_UPDATE;
   // per-group slice, 128-byte aligned (bulk-copy destinations need 16)
   __host__ __device__ static constexpr int per_group() { return (S * OPS * BATW + FPW * WP + 15) / 16 * 16; }
-  static constexpr int YT = BLOCK ? 9 * N2 : 0;      // uniform-grid y^-1 class tables
+  // uniform-grid y^-1 class tables in shared memory; the standalone block preconditioner at
+  // N = 13, 15, 17 reads them through L1 instead, which frees 9 N^2 doubles for a fourth CTA
+  // per SM: p = 12 129 -> 116, p = 14 165 -> 134, p = 16 171 -> 142 us (N = 14 equal, N = 16
+  // 170 -> 189 us: those keep the shared copy)
+#ifdef HDGB_FX_YGLOBAL_N
+  static constexpr bool YGL = FK == FX_PREC && N >= HDGB_FX_YGLOBAL_N;
+#else
+  static constexpr bool YGL = FK == FX_PREC && (N == 13 || N == 15 || N == 17);
+#endif
+  static constexpr int YT = (BLOCK && !YGL) ? 9 * N2 : 0;
   static constexpr int smem_doubles() { return NG * per_group() + (YT + 1) / 2 * 2; }
   // register budget (resident CTAs per SM), measured on the config-3 sweep: 3 for the block
   // preconditioner apply at N >= 8 (p = 8: 130 -> 116 us) and for the staged plain epilogue; 2 for
@@ -277,7 +286,7 @@ struct FxCfg {
 #define HDGB_FX_MINB4_N 11
 #endif
   // N <= 11: 4 CTAs/SM for every kind (block PCG p = 4 744 -> 722, p = 8 772 -> 761, p = 10 789 -> 779 us/iter)
-  static constexpr int MINB = N <= HDGB_FX_MINB4_N ? 4
+  static constexpr int MINB = (N <= HDGB_FX_MINB4_N || YGL) ? 4
                               : (ONE || (FK == FX_POST && !CG && OPS == 2) || (FK == FX_PREC && N >= 8)) ? 3
                               : (FK == FX_UPDATE ? HDGB_FXU_MINB
                                                  : (FK == FX_TRANSFORM && CG ? HDGB_FXT_MINB
@@ -529,9 +538,15 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
       mvA(z, y);
       if (BLOCK) {  // * y^-1 (preconditioner.py:100-104), then pass 3 along the second index
         if (a.ycls) {
-          const double* yi = sY + finfo_cls(inf) * N2 + l * N;
+          if (C::YGL) {
+            const double* yi = a.ycls + finfo_cls(inf) * N2 + l * N;
 #pragma unroll
-          for (int kk = 0; kk < N; ++kk) y[kk] *= yi[kk];
+            for (int kk = 0; kk < N; ++kk) y[kk] *= __ldg(yi + kk);
+          } else {
+            const double* yi = sY + finfo_cls(inf) * N2 + l * N;
+#pragma unroll
+            for (int kk = 0; kk < N; ++kk) y[kk] *= yi[kk];
+          }
         } else {
           const double* yi = a.yfull + (f0 + f) * N2 + l * N;
 #pragma unroll
