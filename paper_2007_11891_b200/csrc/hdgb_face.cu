@@ -263,7 +263,14 @@ struct FxCfg {
 #else
   static constexpr bool YGL = FK == FX_PREC && (N == 13 || N == 15 || N == 17);
 #endif
-  static constexpr int YT = (BLOCK && !YGL) ? 9 * N2 : 0;
+  // same for the fused PCG update at N = 14 and 17 (block PCG p = 13 784 -> 755, p = 16 1001 ->
+  // 957 us/iter; p = 12, 14 equal, p = 15 865 -> 908: shared copy kept)
+#ifdef HDGB_FX_YGLU_N
+  static constexpr bool YGLU = FK == FX_UPDATE && N >= HDGB_FX_YGLU_N;
+#else
+  static constexpr bool YGLU = FK == FX_UPDATE && (N == 14 || N == 17);
+#endif
+  static constexpr int YT = (BLOCK && !YGL && !YGLU) ? 9 * N2 : 0;
   static constexpr int smem_doubles() { return NG * per_group() + (YT + 1) / 2 * 2; }
   // register budget (resident CTAs per SM), measured on the config-3 sweep: 3 for the block
   // preconditioner apply at N >= 8 (p = 8: 130 -> 116 us) and for the staged plain epilogue; 2 for
@@ -286,7 +293,7 @@ struct FxCfg {
 #define HDGB_FX_MINB4_N 11
 #endif
   // N <= 11: 4 CTAs/SM for every kind (block PCG p = 4 744 -> 722, p = 8 772 -> 761, p = 10 789 -> 779 us/iter)
-  static constexpr int MINB = (N <= HDGB_FX_MINB4_N || YGL) ? 4
+  static constexpr int MINB = (N <= HDGB_FX_MINB4_N || YGL || YGLU) ? 4
                               : (ONE || (FK == FX_POST && !CG && OPS == 2) || (FK == FX_PREC && N >= 8)) ? 3
                               : (FK == FX_UPDATE ? HDGB_FXU_MINB
                                                  : (FK == FX_TRANSFORM && CG ? HDGB_FXT_MINB
@@ -538,7 +545,7 @@ __global__ void __launch_bounds__(FxCfg<N, FK, CG>::NT, (FxCfg<N, FK, CG>::MINB)
       mvA(z, y);
       if (BLOCK) {  // * y^-1 (preconditioner.py:100-104), then pass 3 along the second index
         if (a.ycls) {
-          if (C::YGL) {
+          if (C::YGL || C::YGLU) {
             const double* yi = a.ycls + finfo_cls(inf) * N2 + l * N;
 #pragma unroll
             for (int kk = 0; kk < N; ++kk) y[kk] *= __ldg(yi + kk);
