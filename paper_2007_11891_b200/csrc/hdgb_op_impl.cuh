@@ -132,7 +132,11 @@ struct OpVCfg {
 #else
   // register budget (CTAs per SM): measured on the config-3 sweep (p = 2..16)
   static constexpr int MINB = SG ? (512 / NT > 16 ? 16 : 512 / NT)  // 128 registers per thread
-                                 : (SMALL ? 4 : (NT > 256 ? 2 : (N <= 5 ? 3 : (N <= 11 ? 2 : 3))));  // N = 6, 7: 2 (p = 5: 216 -> 210 us)
+                                 : (SMALL ? 4 : (NT > 256 ? 2 : (N <= 5 ? 3 : ((N == 13 || (N == 14 && !PU && !CGT)) ? 3 : 2))));  // N = 6, 7: 2 (p = 5: 216 -> 210 us)
+  // (N = 14..16: 2 since the faces are staged in registers — at 3 CTAs (97 registers) the CG passes
+  // spilled: transformed PCG p = 13 743 -> 628, p = 14 680 -> 609, p = 15 563 -> 521 us/iter,
+  // transformed apply 267 / 298 / 257 -> 271 / 286 / 253 us; N = 14 outside the transformed CG
+  // passes keeps 3: block PCG p = 13 756 -> 801 us/iter with 2)
 #endif
   // staging of the six faces: bulk async copies (TMA unit, one mbarrier per buffer) for
   // N >= HDGB_OPV_TMA_NMIN, per-thread cp.async below.  A face of odd NQ starts on an 8-byte
@@ -344,8 +348,8 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
 // (bulk-copy staging: separate buffer), in slots N (mod 16) doubles apart so lanes of both
 // classes read them without bank conflicts.
 template <int N, int MODE, int COLOR>
-__global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, false, false, (MODE & 32) != 0>::NT,
-                                  OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, false, false, (MODE & 32) != 0>::MINB) opV_kernel(const OpArgs a, int64_t t0, int64_t t1,
+__global__ void __launch_bounds__(OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, false, (MODE & 5) == 1, (MODE & 32) != 0>::NT,
+                                  OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, false, (MODE & 5) == 1, (MODE & 32) != 0>::MINB) opV_kernel(const OpArgs a, int64_t t0, int64_t t1,
                                                           const __grid_constant__ OpVConst<N> K) {
   using C = OpVCfg<N, (MODE & 9) == 9 && COLOR == 0, (MODE & 16) != 0, (MODE & 5) == 1, (MODE & 32) != 0>;
   constexpr int NQ = C::NQ, G = C::G, FS = C::FS, VS = C::VS;
