@@ -132,11 +132,12 @@ struct OpVCfg {
 #else
   // register budget (CTAs per SM): measured on the config-3 sweep (p = 2..16)
   static constexpr int MINB = SG ? (512 / NT > 16 ? 16 : 512 / NT)  // 128 registers per thread
-                                 : (SMALL ? 4 : (NT > 256 ? 2 : (N <= 5 ? 3 : ((N == 13 || (N == 14 && !PU && !CGT)) ? 3 : 2))));  // N = 6, 7: 2 (p = 5: 216 -> 210 us)
+                                 : (SMALL ? 4 : (NT > 256 ? 2 : (N <= 5 ? 3 : (((N == 13 && !PU) || (N == 14 && !PU && !CGT)) ? 3 : 2))));  // N = 6, 7: 2 (p = 5: 216 -> 210 us)
   // (N = 14..16: 2 since the faces are staged in registers — at 3 CTAs (97 registers) the CG passes
   // spilled: transformed PCG p = 13 743 -> 628, p = 14 680 -> 609, p = 15 563 -> 521 us/iter,
   // transformed apply 267 / 298 / 257 -> 271 / 286 / 253 us; N = 14 outside the transformed CG
-  // passes keeps 3: block PCG p = 13 756 -> 801 us/iter with 2)
+  // passes keeps 3: block PCG p = 13 756 -> 801 us/iter with 2; N = 13: 2 for the fused-update
+  // pass only: transformed PCG p = 12 612 -> 554 us/iter, apply and block PCG slower with 2)
 #endif
   // staging of the six faces: bulk async copies (TMA unit, one mbarrier per buffer) for
   // N >= HDGB_OPV_TMA_NMIN, per-thread cp.async below.  A face of odd NQ starts on an 8-byte
